@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse embedding layer step (forward lookup + backward merge + sparse Adagrad
+update) through the C-ABI library, on synthetic BASELINE.json workloads.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1 : workload C2 (BJ:8, the config BASELINE's metric is quoted on): 26 slots x 10M rows/table,
+        D = 64, B = 16,384, Zipf(1.05) ids, element-wise Adagrad, sum pooling.
+N > 1 : workload C3 (BJ:9) row-sharded (cyclic) over N GPUs, B = 16,384 per GPU (weak scaling),
+        launched with torchrun (one process per GPU, NCCL all-to-alls inside libemb).
+--impl reference: the CPU oracle (oracle/, NumPy fp64) timed on the host cores on a bounded sample of
+        the same workload (rank 0 only).
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §7 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synthgen  # noqa: E402
+
+METRIC = "embedding lookups/sec and fwd+bwd+update samples/sec; % of HBM roofline"
+POOL_BATCHES = 16  # distinct staged batches cycled through the timed loop (16 x ~116 MB > 126 MB L2)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy_ r+w)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def workload_for(n_gpus: int):
+    wl = synthgen.WORKLOADS["C2"] if n_gpus == 1 else synthgen.WORKLOADS["C3"]
+    return wl
+
+
+def describe(wl, n):
+    return (f"{wl.name}: {wl.num_slots} slots -> {wl.num_tables} tables, {wl.total_rows:,} rows total, D={wl.dim}, "
+            f"B={wl.batch}/GPU, bag={'U{1..8}' if wl.bag == 'u1_8' else wl.bag_len}, ids={wl.ids}"
+            f"{'(' + str(wl.zipf_s) + ')' if wl.ids == 'zipf' else ''}, {wl.opt}, {wl.pool} pool, "
+            f"{'row-sharded cyclic over ' + str(n) + ' GPUs' if n > 1 else '1 GPU'}")
+
+
+# ------------------------------------------------------------------------------ algorithmic bytes
+def step_bytes(wl, N, SB, U_l, U_o, W):
+    """HBM bytes the method must move per GPU per step."""
+    D = wl.dim
+    k = 16 if wl.opt == "adagrad" else 8
+    fwd = 8 * N + 8 * (SB + 1) + 4 * D * U_o + 4 * D * SB
+    bwd = 4 * D * SB + 8 * N + 8 * (SB + 1) + k * D * U_o
+    return fwd + bwd
+
+
+def kernel_bytes(name, wl, N, SB, U, W):
+    """Algorithmic bytes of one launch of the named kernel."""
+    D = wl.dim
+    if name == "grad_apply":
+        k = 16 if wl.opt == "adagrad" else 8
+        # dY row per occurrence + sorted key/payload/bag index per occurrence + state RMW per touched row
+        return 4 * D * N + 12 * N + k * D * U
+    if name == "pool":
+        # offsets + routing keys + one table row per distinct key + Y write
+        return 8 * (SB + 1) + 4 * N + 4 * D * U + 4 * D * SB
+    return None
+
+
+# ------------------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    def __init__(self, device):
+        self.samples, self.reasons, self.max_mhz, self._stop = [], set(), None, threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, n): n for n in dir(nv) if n.startswith("nvmlClocksEventReason") or
+                 n.startswith("nvmlClocksThrottleReason")}
+        bits = {
+            "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4, "gpu_idle": 0x1,
+            "applications_clocks_setting": 0x2, "sync_boost": 0x10, "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(
+                    nv, "nvmlDeviceGetCurrentClocksEventReasons") else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for n, b in bits.items():
+                    if r & b and n != "gpu_idle":
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "nvml unavailable"}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ CPU oracle timing
+def oracle_time(wl, budget_s=15.0, max_steps=None, batch=None):
+    """Time the oracle (as it stands) on host cores: full steps (lookup + backward + update) of `wl`
+    until `budget_s` of CPU work (bounded sample). Returns (samples/s, sample description)."""
+    from oracle import emb_oracle as O
+    cfg = O.config_from_workload(wl)
+    ora = O.OracleEmbedding(cfg)
+    B = batch or wl.batch
+    done, samples, t_tot, nnz = 0, 0, 0.0, 0
+    k = 0
+    while t_tot < budget_s and (max_steps is None or done < max_steps):
+        bt = synthgen.make_batch(wl, rank=0, step=1000 + k, batch=B)
+        t0 = time.perf_counter()
+        ora.lookup([(bt.ids, bt.offsets, bt.batch)])
+        ora.backward_update([bt.dy], wl.lr)
+        t_tot += time.perf_counter() - t0
+        done += 1
+        samples += B
+        nnz += bt.nnz
+        k += 1
+    return samples / t_tot, nnz / t_tot, f"{done} oracle step(s) of {wl.name} at batch {B} ({t_tot:.1f} s CPU)"
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        n = 1
+    # the oracle's hot NumPy primitives (unique/sort/add.at/fancy indexing) are single-threaded
+    return 1, n
+
+
+# ------------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--workload", default=None, help="override (C1..C5) for experiments")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n = world
+    wl = workload_for(n)
+    if args.workload:
+        wl = synthgen.WORKLOADS[args.workload]
+    if args.batch:
+        wl = wl.with_(batch=args.batch)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        per_step = 9e-5 * 26 / wl.num_slots  # ~s per sample of the oracle (dev-host estimate)
+        B = int(max(64, min(wl.batch, 150.0 / max(1, args.steps + args.warmup) / per_step)))
+        sps, lps, sample = oracle_time(wl, budget_s=1e9, max_steps=args.steps + args.warmup, batch=B)
+        thr, pool = cpu_threads()
+        line = {"impl": "reference", "metric": METRIC, "value": sps, "unit": "samples/s", "n_gpus": n,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * B / sps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": describe(wl, n), "batch_per_step": B},
+                "lookups_per_s": lps,
+                "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": thr, "kind": "oracle",
+                                 "sample": sample + f"; host has {os.cpu_count()} cores"},
+                "e2e": {"value": sps, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    if n > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2112_02752_b200 import emb as E
+    from paper_2112_02752_b200.harness import DeviceBatch, make_layer
+
+    nccl_id = None
+    if n > 1:
+        obj = [E.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    # stage a pool of distinct batches in HBM (inputs resident before the timed region)
+    host_batches = [synthgen.make_batch(wl, rank=rank, step=i) for i in range(POOL_BATCHES)]
+    max_nnz = max(b.nnz for b in host_batches)
+    dev_batches = [DeviceBatch(b, wl.num_slots, wl.dim, local_rank) for b in host_batches]
+    layer = make_layer(wl, max_batch=wl.batch, max_ids=max_nnz, world=n, rank=rank, nccl_id=nccl_id,
+                       device=local_rank)
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        db = dev_batches[i % POOL_BATCHES]
+        layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
+        layer.backward_update(db.dy, wl.lr, stream)
+
+    def barrier():
+        if n > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    # per-step statistics (unique counts) for the byte accounting, outside the timed region
+    infos = []
+    for i in range(POOL_BATCHES):
+        db = dev_batches[i]
+        layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
+        layer.backward_update(db.dy, wl.lr, stream)
+        infos.append(layer.step_info())  # launches counted over lookup + backward
+    barrier()
+
+    layer.profile(True)
+    layer.profile_reset()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(min(args.steps, 64))]
+    barrier()
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            db = dev_batches[i % POOL_BATCHES]
+            if i < len(fwd_ev):
+                fwd_ev[i][0].record(stream)
+            layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
+            if i < len(fwd_ev):
+                fwd_ev[i][1].record(stream)
+            layer.backward_update(db.dy, wl.lr, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    t_ms = ev0.elapsed_time(ev1)
+    prof = layer.profile_read()
+    layer.profile(False)
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
+    if n > 1:
+        t = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+        barrier()
+
+    ms_step = t_ms / args.steps
+    B = wl.batch
+    samples_s = n * B * args.steps / (t_ms / 1e3)
+    mean = lambda key: statistics.mean(inf[key] for inf in infos)  # noqa: E731
+    N_mean = statistics.mean(b.nnz for b in host_batches)
+    SB = wl.num_slots * B
+    U_l, U_o = mean("unique_local"), mean("unique_owner")
+    lookups_s = n * N_mean / (fwd_ms / 1e3)
+    peak, peak_src = _peaks()
+    hbm = step_bytes(wl, N_mean, SB, U_l, U_o, n)
+    launches_per_step = statistics.mean(inf["launches"] for inf in infos)
+
+    # dominant kernel = largest summed device time
+    dom, (dom_ms, dom_cnt) = max(prof.items(), key=lambda kv: kv[1][0])
+    kb = kernel_bytes(dom, wl, N_mean, SB, U_o, n)
+    roof = None
+    if kb is not None and dom_cnt:
+        t_launch = dom_ms / dom_cnt / 1e3
+        ach = kb / t_launch / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "launch_us": round(t_launch * 1e6, 2),
+                "algorithmic_bytes_per_launch": int(kb), "peak_source": peak_src}
+    kernels = {k: {"ms_total": round(v[0], 3), "launches": v[1], "us_per_launch": round(1e3 * v[0] / max(v[1], 1), 2)}
+               for k, v in prof.items()}
+
+    # e2e through the host-buffer C-ABI entry points (pinned host memory, copies inside the timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        hb = host_batches[0]
+        ids_h = torch.from_numpy(hb.ids).pin_memory()
+        off_h = torch.from_numpy(hb.offsets).pin_memory()
+        dy_h = torch.from_numpy(hb.dy).pin_memory()
+        out_h = torch.empty((B, wl.num_slots, wl.dim), dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            layer.lookup_host(ids_h.numpy(), off_h.numpy(), B, hb.nnz, out_h.numpy(), stream)
+            layer.backward_update_host(dy_h.numpy(), wl.lr, stream)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            layer.lookup_host(ids_h.numpy(), off_h.numpy(), B, hb.nnz, out_h.numpy(), stream)
+            layer.backward_update_host(dy_h.numpy(), wl.lr, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1)
+        if n > 1:
+            t = torch.tensor([te], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": n * B * args.e2e_steps / (te / 1e3), "unit": "samples/s",
+               "h2d_bytes_per_step": int(hb.ids.nbytes + hb.offsets.nbytes + hb.dy.nbytes),
+               "d2h_bytes_per_step": int(out_h.numel() * 4), "ms_per_step": te / args.e2e_steps,
+               "path": "emb_lookup_host + emb_backward_update_host (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        sps, lps, sample = oracle_time(wl, budget_s=args.cpu_budget)
+        thr, pool = cpu_threads()
+        cpu = {"value": sps, "unit": "samples/s", "cores": thr, "kind": "oracle",
+               "sample": sample + f"; host has {os.cpu_count()} cores, NumPy primitives single-threaded",
+               "lookups_per_s": lps}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": samples_s, "unit": "samples/s", "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (fp64 accumulation)", "data": "synthetic",
+            "config": {"workload": describe(wl, n), "global_batch": n * B, "nnz_per_gpu": N_mean,
+                       "unique_local": U_l, "unique_owner": U_o,
+                       "l2": f"inputs larger than L2: {POOL_BATCHES} distinct staged batches cycled "
+                             f"({POOL_BATCHES} x {(hb_bytes(host_batches[0], wl)) / 1e6:.0f} MB) + "
+                             f"{layer.rows_local * wl.dim * 4 * (2 if wl.opt == 'adagrad' else 1) / 1e9:.1f} GB table "
+                             "state per GPU"},
+            "lookups_per_s": lookups_s,
+            "fwd_ms": fwd_ms,
+            "step_roofline": {"bound": "hbm", "algorithmic_bytes": int(hbm),
+                              "achieved": round(hbm / (ms_step / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                              "frac": round(hbm / (ms_step / 1e3) / 1e9 / peak, 4)},
+            "roofline": roof,
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if n > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def hb_bytes(bt, wl):
+    return bt.ids.nbytes + bt.offsets.nbytes + bt.dy.nbytes + bt.batch * wl.num_slots * wl.dim * 4
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+// internal.h — host-side declarations shared by the libemb translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace emb {
+
+// Sharding / key-space parameters (R7). The ROUTING KEY of a fused row g is
+//   W == 1 : rk = g
+//   W  > 1 : rk = owner(g) << lbits | local(g)
+// so sorting routing keys groups the unique keys by owner, ascending local id within an owner.
+struct KeySpace {
+  int32_t world;
+  int32_t rank;
+  int32_t shard;       // 0 cyclic, 1 block
+  uint32_t lbits;      // bits of the local row id (W > 1)
+  uint64_t rows_per;   // block sharding: ceil(R_total / W)
+  uint32_t key_bits;   // bits the radix sort must look at (sentinel strictly above every valid key)
+};
+
+__host__ __device__ inline uint32_t route_key(uint64_t g, const KeySpace &ks) {
+  if (ks.world == 1) return (uint32_t)g;
+  uint64_t owner, local;
+  if (ks.shard == 0) {
+    owner = g % (uint64_t)ks.world;
+    local = g / (uint64_t)ks.world;
+  } else {
+    owner = g / ks.rows_per;
+    local = g % ks.rows_per;
+  }
+  return (uint32_t)((owner << ks.lbits) | local);
+}
+__host__ __device__ inline uint64_t key_to_global(uint32_t rk, const KeySpace &ks) {
+  if (ks.world == 1) return rk;
+  uint64_t owner = rk >> ks.lbits, local = rk & ((1u << ks.lbits) - 1u);
+  return ks.shard == 0 ? local * (uint64_t)ks.world + owner : owner * ks.rows_per + local;
+}
+
+// kernel ids for the per-kernel event profiler (order = emb_profile_name)
+enum KernelId {
+  KID_KEYS = 0,
+  KID_SORT_HIST,
+  KID_SORT_PASS,
+  KID_POOL,
+  KID_GRAD_APPLY,
+  KID_UNIQUE,
+  KID_ROUTE,
+  KID_OWNER_GATHER,
+  KID_GRAD_LOCAL,
+  KID_NCCL,
+  KID_INIT,
+  KID_COUNT
+};
+
+// ---- launchers (each returns cudaGetLastError()) ------------------------------------------------
+struct KeysArgs {
+  const int64_t *ids;
+  const int64_t *offsets;
+  int64_t nnz;
+  int32_t batch;
+  int32_t num_slots;
+  const int32_t *slot_table;  // device [S]
+  const uint64_t *base;       // device [T]
+  const int64_t *rows;        // device [T]
+  KeySpace ks;
+  uint32_t *key;     // out [nnz] routing key or EMB_SENTINEL
+  uint32_t *bag_of;  // out [nnz] bag index s*B+b
+  int32_t *blen;     // out [S*B] bag length
+  uint32_t *err;     // sticky device error word
+};
+cudaError_t launch_keys(const KeysArgs &a, cudaStream_t st);
+
+// stable LSD radix sort of (key, value) pairs on the low `key_bits` bits. Input (kin, vin) is left
+// untouched; vin == nullptr means value = index. Result lands in (*keys_out, *vals_out), one of the
+// two scratch pairs (k0, v0) / (k1, v1).
+struct SortWorkspace {
+  uint32_t *hist;      // [4][256]
+  uint32_t *counters;  // [4]
+  uint32_t *status;    // [4][max_tiles][256]
+  int64_t max_tiles;
+  uint32_t *err;       // sticky device error word (internal bounds guard)
+};
+size_t sort_workspace_words(int64_t max_n);
+typedef void (*ProfHook)(void *ctx, int kid, int end, cudaStream_t st);
+cudaError_t radix_sort_pairs(const SortWorkspace &ws, const uint32_t *kin, const uint32_t *vin, uint32_t *k0,
+                             uint32_t *v0, uint32_t *k1, uint32_t *v1, int64_t n, uint32_t key_bits,
+                             cudaStream_t st, uint32_t **keys_out, uint32_t **vals_out, int *launches,
+                             ProfHook prof, void *prof_ctx);
+
+// W == 1 forward: Y[b][s][:] = pool over bag of table rows, straight from the table.
+struct PoolArgs {
+  const uint32_t *key;     // [nnz] routing keys in CSR order (EMB_SENTINEL = skip)
+  const int64_t *offsets;  // [S*B+1]
+  int64_t nnz;
+  int32_t batch, num_slots, dim;
+  int32_t mean;
+  const float *rows_src;   // table (W==1) or received unique rows (W>1)
+  int64_t nrows_src;       // rows in rows_src (bounds guard)
+  const uint32_t *row_idx; // nullptr: row = key (W==1); else row = row_idx[j] (inverse -> unique index)
+  float *out;
+  uint32_t *err;           // device error word (copied to err_host by block 0)
+  uint32_t *err_host;      // mapped pinned host word (may be null)
+};
+cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st);
+
+// backward: segment reduce over sorted (key, pay) + sink
+struct GradArgs {
+  const uint32_t *skey;    // [n] sorted routing keys (sentinel last)
+  const uint32_t *spay;    // [n] payload (occurrence index j, or receive slot)
+  int64_t n;
+  int32_t dim;
+  // contribution source: mode 0 = dY rows via bag_of/blen; mode 1 = rows of `src` at index spay
+  int32_t src_mode;
+  const float *dy;         // [B][S][D]
+  const uint32_t *bag_of;  // [nnz]
+  int64_t nsrc_occ;        // entries of bag_of (bounds guard)
+  const int32_t *blen;     // [S*B] (mean) or nullptr
+  int32_t batch, num_slots;
+  const float *src;        // mode 1
+  // sink: mode 0 = optimizer apply on table rows (local row = key & lmask); mode 1 = write fp32 row
+  // to out_rows[useg[p]] (requester-side local grad)
+  int32_t sink_mode;
+  uint32_t lmask;
+  int32_t opt;             // 0 sgd 1 adagrad
+  double lr, eps;
+  float *w, *a;
+  int64_t nrows;           // rows of w/a (bounds guard)
+  int64_t nsrc;            // rows of dy (S*B) or src (bounds guard)
+  int64_t nout;            // rows of out_rows (bounds guard)
+  uint32_t *err;
+  const uint32_t *useg;    // sink mode 1: unique index per sorted position
+  float *out_rows;
+  double *partials;        // [2*nchunks][D]
+  uint32_t *tickets;       // [nchunks], zero on entry, left zero
+};
+cudaError_t launch_grad(const GradArgs &a, cudaStream_t st);
+
+// dedup of sorted keys: useg[p] = unique index of sorted position p, ukey[u], ustart[u] (ustart[U]
+// = number of valid positions), *u_count (device).
+struct UniqueArgs {
+  const uint32_t *skey;
+  int64_t n;
+  uint32_t *useg, *ukey, *ustart, *u_count;
+  uint32_t *status;  // [tiles] zeroed
+  uint32_t *counter; // zeroed
+};
+size_t unique_status_words(int64_t max_n);
+cudaError_t launch_unique(const UniqueArgs &a, cudaStream_t st);
+
+// table init (R15) and row helpers
+cudaError_t launch_init(float *w, float *a, int64_t rows_local, int32_t dim, uint64_t seed, float init_accum,
+                        const KeySpace &ks, int32_t rank, cudaStream_t st);
+cudaError_t launch_rows_gather(const float *src, const int64_t *rows, int64_t n, int32_t dim, float *dst,
+                               cudaStream_t st);
+cudaError_t launch_rows_scatter(float *dst, const int64_t *rows, int64_t n, int32_t dim, const float *src,
+                                cudaStream_t st);
+
+// W > 1 helpers
+cudaError_t launch_owner_counts(const uint32_t *ukey, const uint32_t *u_count, int32_t world, uint32_t lbits,
+                                int64_t *send_counts, cudaStream_t st);
+cudaError_t launch_scatter_inverse(const uint32_t *spay, const uint32_t *useg, int64_t n, uint32_t *inv,
+                                   const uint32_t *u_count, const uint32_t *ustart, cudaStream_t st);
+cudaError_t launch_local_of_unique(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, uint32_t lmask,
+                                   uint32_t *out, cudaStream_t st);
+cudaError_t launch_owner_gather(const float *w, const uint32_t *local, int64_t n, int32_t dim, float *out,
+                                cudaStream_t st);
+
+}  // namespace emb

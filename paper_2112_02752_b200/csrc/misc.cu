@@ -1,0 +1,239 @@
+// misc.cu — dedup compaction (A2), owner routing helpers (A3/A5), owner-side row gather (A6 at
+// W > 1), table init (R15) and row export/import kernels.
+#include "common.cuh"
+#include "internal.h"
+
+namespace emb {
+
+// ------------------------------------------------------------------------------------------------
+// k_unique: segment heads of the sorted key array -> unique index per position (useg), unique keys
+// (ukey), segment starts (ustart, with ustart[U] = #valid), U. One tile of 4096 positions per CTA,
+// 512 threads x 8 consecutive positions; tile prefix by decoupled look-back (tiles claimed in order).
+namespace {
+constexpr int UQ_THREADS = 512;
+constexpr int UQ_ITEMS = 8;
+constexpr int UQ_TILE = UQ_THREADS * UQ_ITEMS;
+constexpr uint32_t UF_AGG = 1u << 30, UF_INC = 2u << 30, UF_MASK = (1u << 30) - 1u;
+}  // namespace
+
+size_t unique_status_words(int64_t max_n) { return (size_t)((max_n + UQ_TILE - 1) / UQ_TILE + 1) + 1; }
+
+__global__ void __launch_bounds__(UQ_THREADS) k_unique(UniqueArgs a) {
+  __shared__ uint32_t s_tile, s_excl;
+  __shared__ uint32_t warp_tot[UQ_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(a.counter, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * UQ_TILE + (int64_t)tid * UQ_ITEMS;
+  uint32_t k[UQ_ITEMS];
+  uint32_t prev = 0;
+  if (base > 0 && base - 1 < a.n) prev = a.skey[base - 1];
+#pragma unroll
+  for (int i = 0; i < UQ_ITEMS; ++i) k[i] = (base + i < a.n) ? a.skey[base + i] : EMB_SENTINEL;
+  uint32_t flags = 0, cnt = 0;
+#pragma unroll
+  for (int i = 0; i < UQ_ITEMS; ++i) {
+    const uint32_t kp = i == 0 ? prev : k[i - 1];
+    const bool h = k[i] != EMB_SENTINEL && (base + i == 0 || k[i] != kp);
+    flags |= (uint32_t)h << i;
+    cnt += h;
+  }
+  // block exclusive scan of cnt
+  uint32_t incl = warp_incl_scan(cnt);
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = lane < UQ_THREADS / 32 ? warp_tot[lane] : 0;
+    uint32_t ti = warp_incl_scan(t);
+    if (lane < UQ_THREADS / 32) warp_tot[lane] = ti - t;  // exclusive warp offsets
+    const uint32_t total = __shfl_sync(0xffffffffu, ti, UQ_THREADS / 32 - 1);
+    if (lane == 0) {
+      volatile uint32_t *st = a.status + tile;
+      uint32_t excl = 0;
+      if (tile == 0) {
+        *st = UF_INC | total;
+      } else {
+        *st = UF_AGG | total;
+        int64_t look = tile - 1;
+        while (true) {
+          uint32_t s;
+          do {
+            s = *(volatile uint32_t *)(a.status + look);
+          } while ((s & ~UF_MASK) == 0);
+          excl += s & UF_MASK;
+          if (s & UF_INC) break;
+          --look;
+        }
+        *st = UF_INC | (excl + total);
+      }
+      s_excl = excl;
+    }
+  }
+  __syncthreads();
+  uint32_t u = s_excl + warp_tot[w] + (incl - cnt);  // heads before my first position
+#pragma unroll
+  for (int i = 0; i < UQ_ITEMS; ++i) {
+    const int64_t p = base + i;
+    if (p >= a.n || k[i] == EMB_SENTINEL) break;
+    if ((flags >> i) & 1u) {
+      a.ukey[u] = k[i];
+      a.ustart[u] = (uint32_t)p;
+      ++u;
+    }
+    a.useg[p] = u - 1;
+    const uint32_t kn = (i + 1 < UQ_ITEMS) ? k[i + 1] : ((p + 1 < a.n) ? a.skey[p + 1] : EMB_SENTINEL);
+    if (kn == EMB_SENTINEL) {  // last valid position of the whole array
+      a.ustart[u] = (uint32_t)(p + 1);
+      *a.u_count = u;
+    }
+  }
+  if (tile == 0 && tid == 0 && (a.n == 0 || k[0] == EMB_SENTINEL)) {
+    a.ustart[0] = 0;
+    *a.u_count = 0;
+  }
+}
+
+cudaError_t launch_unique(const UniqueArgs &a, cudaStream_t st) {
+  const int64_t tiles = a.n > 0 ? (a.n + UQ_TILE - 1) / UQ_TILE : 1;
+  cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(a.status, 0, sizeof(uint32_t) * (size_t)tiles, st);
+  if (e != cudaSuccess) return e;
+  k_unique<<<(unsigned)tiles, UQ_THREADS, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------------
+// owner routing helpers (W > 1)
+__global__ void k_owner_counts(const uint32_t *ukey, const uint32_t *u_count, int32_t world, uint32_t lbits,
+                               int64_t *send_counts) {
+  const int d = threadIdx.x;
+  if (d >= world) return;
+  const int64_t U = *u_count;
+  auto lb = [&](uint64_t x) {
+    int64_t lo = 0, hi = U;
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if ((uint64_t)ukey[m] < x) lo = m + 1; else hi = m;
+    }
+    return lo;
+  };
+  send_counts[d] = lb((uint64_t)(d + 1) << lbits) - lb((uint64_t)d << lbits);
+}
+cudaError_t launch_owner_counts(const uint32_t *ukey, const uint32_t *u_count, int32_t world, uint32_t lbits,
+                                int64_t *send_counts, cudaStream_t st) {
+  k_owner_counts<<<1, 32, 0, st>>>(ukey, u_count, world, lbits, send_counts);
+  return cudaGetLastError();
+}
+
+__global__ void k_scatter_inverse(const uint32_t *spay, const uint32_t *useg, int64_t n, uint32_t *inv,
+                                  const uint32_t *u_count, const uint32_t *ustart) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t nvalid = ustart[*u_count];
+  inv[spay[p]] = (uint32_t)p < nvalid ? useg[p] : EMB_SENTINEL;
+}
+cudaError_t launch_scatter_inverse(const uint32_t *spay, const uint32_t *useg, int64_t n, uint32_t *inv,
+                                   const uint32_t *u_count, const uint32_t *ustart, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_scatter_inverse<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(spay, useg, n, inv, u_count, ustart);
+  return cudaGetLastError();
+}
+
+__global__ void k_local_of_unique(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, uint32_t lmask,
+                                  uint32_t *out) {
+  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= cap || u >= (int64_t)*u_count) return;
+  out[u] = ukey[u] & lmask;
+}
+cudaError_t launch_local_of_unique(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, uint32_t lmask,
+                                   uint32_t *out, cudaStream_t st) {
+  if (cap <= 0) return cudaSuccess;
+  k_local_of_unique<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(ukey, u_count, cap, lmask, out);
+  return cudaGetLastError();
+}
+
+// owner-side gather: out[i][:] = w[local[i]][:] (float4 per thread, a row per D/4 threads)
+__global__ void k_owner_gather(const float4 *__restrict__ w, const uint32_t *__restrict__ local, int64_t n, int d4,
+                               float4 *__restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = t / d4;
+  const int c = (int)(t - i * d4);
+  if (i >= n) return;
+  out[t] = ld_nc_f4(w + (size_t)local[i] * d4 + c);
+}
+cudaError_t launch_owner_gather(const float *w, const uint32_t *local, int64_t n, int32_t dim, float *out,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int d4 = dim / 4;
+  const int64_t total = n * d4;
+  k_owner_gather<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(reinterpret_cast<const float4 *>(w), local, n,
+                                                                  d4, reinterpret_cast<float4 *>(out));
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------------
+// table init (R15): w[g][c] = int16(splitmix64(seed ^ (g*D + c)) >> 48) * 2^-19, a = init_accum
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void k_init(float4 *w, float4 *a, int64_t rows_local, int d4, uint64_t seed, float init_accum,
+                       KeySpace ks, int32_t rank) {
+  const int64_t total = rows_local * d4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t D = (uint64_t)d4 * 4;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int64_t r = t / d4;
+    const int c4 = (int)(t - r * d4);
+    uint64_t g;
+    if (ks.world == 1) g = (uint64_t)r;
+    else if (ks.shard == 0) g = (uint64_t)r * (uint64_t)ks.world + (uint64_t)rank;
+    else g = (uint64_t)rank * ks.rows_per + (uint64_t)r;
+    float v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t h = splitmix64(seed ^ (g * D + (uint64_t)(c4 * 4 + q)));
+      v[q] = (float)(int16_t)(uint16_t)(h >> 48) * 0x1p-19f;
+    }
+    w[t] = make_float4(v[0], v[1], v[2], v[3]);
+    if (a) a[t] = make_float4(init_accum, init_accum, init_accum, init_accum);
+  }
+}
+cudaError_t launch_init(float *w, float *a, int64_t rows_local, int32_t dim, uint64_t seed, float init_accum,
+                        const KeySpace &ks, int32_t rank, cudaStream_t st) {
+  if (rows_local <= 0) return cudaSuccess;
+  k_init<<<148 * 8, 256, 0, st>>>(reinterpret_cast<float4 *>(w), reinterpret_cast<float4 *>(a), rows_local, dim / 4,
+                                  seed, init_accum, ks, rank);
+  return cudaGetLastError();
+}
+
+__global__ void k_rows_copy(const float4 *src, float4 *dst, const int64_t *rows, int64_t n, int d4, int gather) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = t / d4;
+  const int c = (int)(t - i * d4);
+  if (i >= n) return;
+  if (gather) dst[t] = src[(size_t)rows[i] * d4 + c];
+  else dst[(size_t)rows[i] * d4 + c] = src[t];
+}
+cudaError_t launch_rows_gather(const float *src, const int64_t *rows, int64_t n, int32_t dim, float *dst,
+                               cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int d4 = dim / 4;
+  k_rows_copy<<<(unsigned)((n * d4 + 255) / 256), 256, 0, st>>>(reinterpret_cast<const float4 *>(src),
+                                                                reinterpret_cast<float4 *>(dst), rows, n, d4, 1);
+  return cudaGetLastError();
+}
+cudaError_t launch_rows_scatter(float *dst, const int64_t *rows, int64_t n, int32_t dim, const float *src,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int d4 = dim / 4;
+  k_rows_copy<<<(unsigned)((n * d4 + 255) / 256), 256, 0, st>>>(reinterpret_cast<const float4 *>(src),
+                                                                reinterpret_cast<float4 *>(dst), rows, n, d4, 0);
+  return cudaGetLastError();
+}
+
+}  // namespace emb

@@ -1,0 +1,307 @@
+"""GPU parity of the CUDA path (through the C-ABI) against the CPU oracle, element by element on the
+same seeded inputs. Tolerance (BJ:5 / R21): |gpu - oracle| <= 1e-6 + 1e-5*|oracle| for pooled
+outputs and updated rows; unique sets, counts and routing bit-exact; run-to-run bitwise determinism.
+Multi-step comparisons follow the stepwise-resynced protocol (R22) unless stated free-running."""
+import numpy as np
+import pytest
+
+import synthgen
+from oracle import emb_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-6
+
+
+@pytest.fixture(scope="module")
+def torch():
+    t = pytest.importorskip("torch")
+    if not t.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2112_02752_b200 import build
+    build.build()
+    return t
+
+
+def _layer(wl, B, nnz_cap, **kw):
+    from paper_2112_02752_b200.harness import make_layer
+    return make_layer(wl, max_batch=B, max_ids=max(nnz_cap, 1), **kw)
+
+
+def _run_step(torch, layer, bt, lr, dy=None):
+    from paper_2112_02752_b200.harness import DeviceBatch
+    db = DeviceBatch(bt, layer.num_slots, layer.dim, layer.device)
+    layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out)
+    torch.cuda.synchronize()
+    Y = db.out.cpu().numpy()
+    info = layer.step_info()
+    keys, counts = layer.last_unique()
+    d = db.dy if dy is None else torch.from_numpy(dy).cuda()
+    layer.backward_update(d, lr)
+    torch.cuda.synchronize()
+    return Y, info, keys, counts
+
+
+def _touched_rows(cfg, bt):
+    g, _, _ = O.occurrence_keys(cfg, bt.ids, bt.offsets, bt.batch)
+    return np.unique(g)
+
+
+def _read_global(layer, cfg, g):
+    """Read fused rows g (all owned by this W=1 layer) -> (w, a)."""
+    t = np.searchsorted(cfg.base, g, side="right") - 1
+    w = np.empty((g.size, cfg.dim), np.float32)
+    a = np.empty((g.size, cfg.dim), np.float32)
+    for tt in np.unique(t):
+        m = t == tt
+        w[m], a[m] = layer.read_rows(int(tt), g[m] - cfg.base[tt])
+    return w, a
+
+
+def _check_close(gpu, ref, what):
+    err = np.abs(gpu.astype(np.float64) - ref.astype(np.float64))
+    bound = ATOL + RTOL * np.abs(ref.astype(np.float64))
+    bad = err > bound
+    assert not bad.any(), f"{what}: {bad.sum()} elements out of tolerance, worst {np.max(err / bound):.3g}x"
+
+
+def _parity_run(torch, wl, B, steps, lr, resync=True, empty_frac=0.0, check_all_rows=False):
+    cfg = O.config_from_workload(wl)
+    bts = [synthgen.make_batch(wl, step=k, batch=B, empty_frac=empty_frac) for k in range(steps)]
+    layer = _layer(wl, B, max(bt.nnz for bt in bts))
+    ora = O.OracleEmbedding(cfg)
+    try:
+        for k, bt in enumerate(bts):
+            touched = _touched_rows(cfg, bt)
+            if resync and k > 0:
+                w, a = _read_global(layer, cfg, touched)
+                ora.load_rows(touched, w, a)
+            Y, info, keys, counts = _run_step(torch, layer, bt, lr)
+            (Yo,) = ora.lookup([(bt.ids, bt.offsets, bt.batch)])
+            _check_close(Y, Yo, f"Y step {k}")
+            g, _, _ = O.occurrence_keys(cfg, bt.ids, bt.offsets, bt.batch)
+            Uo, co, _ = O.dedup(g)
+            assert np.array_equal(keys.astype(np.int64), Uo), "unique set differs"
+            assert np.array_equal(counts, co), "counts differ"
+            assert info["unique_local"] == Uo.size and info["nnz"] == bt.nnz
+            ora.backward_update([bt.dy], lr)
+            rows = np.arange(cfg.total_rows) if check_all_rows else touched
+            w, a = _read_global(layer, cfg, rows)
+            wo, ao = ora.rows(rows)
+            _check_close(w, wo, f"w step {k}")
+            if wl.opt == "adagrad":
+                _check_close(a, ao, f"a step {k}")
+    finally:
+        layer.close()
+
+
+# ----------------------------------------------------------------------------- C1 (BJ:7) and variants
+def test_c1_full_config_free_running(torch):
+    """C1 exactly as BJ:7 (uniform ids, SGD, sum): free-running 4 steps, whole table compared."""
+    wl = synthgen.WORKLOADS["C1"]
+    _parity_run(torch, wl, wl.batch, steps=4, lr=wl.lr, resync=False, check_all_rows=True)
+
+
+@pytest.mark.parametrize("pool", ["sum", "mean"])
+@pytest.mark.parametrize("opt", ["sgd", "adagrad"])
+def test_c1_pool_opt_matrix(torch, pool, opt):
+    wl = synthgen.WORKLOADS["C1"].with_(pool=pool, opt=opt, ids="zipf", zipf_s=1.2)
+    _parity_run(torch, wl, 777, steps=3, lr=0.05, empty_frac=0.1)
+
+
+@pytest.mark.parametrize("dim", [4, 16, 64, 100, 128, 256])
+def test_dims(torch, dim):
+    wl = synthgen.WORKLOADS["C1"].with_(dim=dim, rows=(5000, 3000), slot_table=(0, 1, 1), ids="zipf", zipf_s=1.1,
+                                        opt="adagrad", pool="mean")
+    _parity_run(torch, wl, 300, steps=2, lr=0.1, empty_frac=0.05)
+
+
+def test_c2_reduced_batch_full_tables(torch):
+    """C2 tables (26 x 10M, D=64, Zipf 1.05, Adagrad) with a reduced batch: 3 resynced steps."""
+    wl = synthgen.WORKLOADS["C2"]
+    _parity_run(torch, wl, 1024, steps=3, lr=wl.lr)
+
+
+def test_c5_hot_ids_reduced(torch):
+    """C5 hot-id stress (bag 64, 90% of ids in the top-1k rows per table) at one rank, B=256:
+    long duplicate segments exercise the multi-chunk ticket combine."""
+    wl = synthgen.WORKLOADS["C5"]
+    _parity_run(torch, wl, 256, steps=2, lr=wl.lr)
+
+
+# ----------------------------------------------------------------------------- edge cases
+def _hand_batch(ids, offsets, B, S, D, seed=0):
+    rng = np.random.default_rng(seed)
+    return synthgen.Batch(ids=np.asarray(ids, np.int64), offsets=np.asarray(offsets, np.int64), batch=B,
+                          dy=(rng.random((B, S, D), dtype=np.float32) * 2 - 1).astype(np.float32))
+
+
+def _edge_run(torch, wl, bt, lr=0.1, steps=1):
+    cfg = O.config_from_workload(wl)
+    layer = _layer(wl, max(bt.batch, 1), max(bt.nnz, 1))
+    ora = O.OracleEmbedding(cfg)
+    try:
+        for _ in range(steps):
+            Y, info, keys, counts = _run_step(torch, layer, bt, lr)
+            (Yo,) = ora.lookup([(bt.ids, bt.offsets, bt.batch)])
+            _check_close(Y, Yo, "Y")
+            ora.backward_update([bt.dy], lr)
+            rows = np.arange(cfg.total_rows)
+            w, a = _read_global(layer, cfg, rows)
+            _check_close(w, ora.rows(rows)[0], "w")
+    finally:
+        layer.close()
+
+
+def test_one_id_repeated_many_times(torch):
+    """A single row hit 5000 times (a segment spanning ~157 chunks) plus a few others."""
+    wl = synthgen.WORKLOADS["C1"].with_(rows=(64,), slot_table=(0,), dim=16, opt="adagrad")
+    ids = np.concatenate([np.full(5000, 7), np.arange(20) % 64, np.full(100, 63)])
+    B = 50
+    lens = np.full(B, ids.size // B)
+    lens[-1] += ids.size - lens.sum()
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    _edge_run(torch, wl, _hand_batch(ids, offs, B, 1, 16), steps=2)
+
+
+def test_all_empty_bags_and_max_id(torch):
+    wl = synthgen.WORKLOADS["C1"].with_(rows=(10, 5), slot_table=(0, 1), dim=8, opt="sgd")
+    ids = np.array([9, 4, 4, 0])
+    offs = np.array([0, 0, 0, 2, 2, 2, 4])  # S=2, B=3: bags (0,0)=[], (0,1)=[], (0,2)=[9,4], (1,*)=[],[],[4,0]
+    _edge_run(torch, wl, _hand_batch(ids, offs, 3, 2, 8))
+
+
+def test_batch_zero_and_nnz_zero(torch):
+    wl = synthgen.WORKLOADS["C1"].with_(rows=(10,), slot_table=(0,), dim=8)
+    _edge_run(torch, wl, _hand_batch([], [0, 0, 0, 0], 3, 1, 8))
+    layer = _layer(wl, 4, 4)
+    try:
+        out = torch.empty((0, 1, 8), device="cuda")
+        layer.lookup(torch.zeros(1, dtype=torch.int64, device="cuda"),
+                     torch.zeros(1, dtype=torch.int64, device="cuda"), 0, 0, out)
+        layer.backward_update(out, 0.1)
+        torch.cuda.synchronize()
+    finally:
+        layer.close()
+
+
+def test_determinism_bitwise(torch):
+    wl = synthgen.WORKLOADS["C5"].with_(rows=(200_000,) * 4, slot_table=(0, 1, 2, 3), bag_len=32)
+    bts = [synthgen.make_batch(wl, step=k, batch=512) for k in range(2)]
+    res = []
+    for _ in range(2):
+        layer = _layer(wl, 512, bts[0].nnz)
+        Ys = [_run_step(torch, layer, bt, 0.01)[0] for bt in bts]
+        g = np.arange(0, 200_000, 7)
+        w, a = layer.read_rows(1, g)
+        res.append((Ys, w, a))
+        layer.close()
+    for y0, y1 in zip(res[0][0], res[1][0]):
+        assert np.array_equal(y0.view(np.uint32), y1.view(np.uint32))
+    assert np.array_equal(res[0][1].view(np.uint32), res[1][1].view(np.uint32))
+    assert np.array_equal(res[0][2].view(np.uint32), res[1][2].view(np.uint32))
+
+
+def test_first_forward_bit_exact(torch):
+    """R15: with the hash init every partial sum is exact in fp32, so step 0's Y is bit-exact."""
+    wl = synthgen.WORKLOADS["C2"]
+    cfg = O.config_from_workload(wl)
+    bt = synthgen.make_batch(wl, batch=2048)
+    layer = _layer(wl, 2048, bt.nnz)
+    try:
+        Y, *_ = _run_step(torch, layer, bt, 0.0)
+    finally:
+        layer.close()
+    (Yo,) = O.OracleEmbedding(cfg).lookup([(bt.ids, bt.offsets, bt.batch)])
+    assert np.array_equal(Y.view(np.uint32), Yo.view(np.uint32))
+
+
+# ----------------------------------------------------------------------------- errors and protocol
+def test_out_of_range_id_sticky_and_no_update(torch):
+    from paper_2112_02752_b200.emb import EmbError, EMB_ERR_RANGE
+    wl = synthgen.WORKLOADS["C1"].with_(rows=(10,), slot_table=(0,), dim=8, opt="sgd")
+    layer = _layer(wl, 4, 8)
+    try:
+        w0, _ = layer.read_rows(0, np.arange(10))
+        bt = _hand_batch([1, 10, 3], [0, 2, 3], 2, 1, 8)
+        from paper_2112_02752_b200.harness import DeviceBatch
+        db = DeviceBatch(bt, 1, 8)
+        layer.lookup(db.ids, db.offsets, 2, 3, db.out)
+        torch.cuda.synchronize()
+        with pytest.raises(EmbError) as ei:
+            layer.backward_update(db.dy, 0.1)
+        assert ei.value.status == EMB_ERR_RANGE
+        # the bad id contributed nothing to the forward: bag 0 = row 1 only
+        np.testing.assert_array_equal(db.out.cpu().numpy()[0, 0], w0[1])
+        with pytest.raises(EmbError):
+            layer.lookup(db.ids, db.offsets, 2, 3, db.out)
+        layer.clear_error()
+        w1, _ = layer.read_rows(0, np.arange(10))
+        assert np.array_equal(w0, w1)
+    finally:
+        layer.close()
+
+
+def test_bad_offsets_and_state_errors(torch):
+    from paper_2112_02752_b200.emb import EmbError, EMB_ERR_INVALID, EMB_ERR_STATE
+    wl = synthgen.WORKLOADS["C1"].with_(rows=(10,), slot_table=(0,), dim=8)
+    layer = _layer(wl, 4, 8)
+    try:
+        from paper_2112_02752_b200.harness import DeviceBatch
+        with pytest.raises(EmbError) as ei:
+            layer.backward_update(torch.zeros(8, device="cuda"), 0.1)
+        assert ei.value.status == EMB_ERR_STATE
+        db = DeviceBatch(_hand_batch([1, 2, 3], [0, 2, 1, 3], 3, 1, 8), 1, 8)
+        layer.lookup(db.ids, db.offsets, 3, 3, db.out)
+        torch.cuda.synchronize()
+        with pytest.raises(EmbError) as ei:
+            layer.backward_update(db.dy, 0.1)
+        assert ei.value.status == EMB_ERR_INVALID
+        layer.clear_error()
+        with pytest.raises(EmbError) as ei:  # argument error: nnz above capacity
+            layer.lookup(db.ids, db.offsets, 3, 9, db.out)
+        assert ei.value.status == EMB_ERR_INVALID
+        db2 = DeviceBatch(_hand_batch([1, 2, 3], [0, 1, 2, 3], 3, 1, 8), 1, 8)
+        layer.lookup(db2.ids, db2.offsets, 3, 3, db2.out)
+        with pytest.raises(EmbError) as ei:
+            layer.lookup(db2.ids, db2.offsets, 3, 3, db2.out)
+        assert ei.value.status == EMB_ERR_STATE
+    finally:
+        layer.close()
+
+
+def test_read_write_rows_roundtrip_bitwise(torch):
+    wl = synthgen.WORKLOADS["C1"].with_(rows=(1000, 500), slot_table=(0, 1), dim=16, opt="adagrad")
+    layer = _layer(wl, 8, 64)
+    try:
+        rows = np.array([0, 5, 499])
+        w = np.random.default_rng(0).random((3, 16), dtype=np.float32)
+        a = np.random.default_rng(1).random((3, 16), dtype=np.float32)
+        layer.write_rows(1, rows, w, a)
+        w2, a2 = layer.read_rows(1, rows)
+        assert np.array_equal(w, w2) and np.array_equal(a, a2)
+        w0, _ = layer.read_rows(0, rows)
+        cfg = O.config_from_workload(wl)
+        assert np.array_equal(w0, O.init_weights(cfg.seed, rows, 16))  # hash init bitwise (R15)
+    finally:
+        layer.close()
+
+
+def test_host_buffer_path(torch):
+    wl = synthgen.WORKLOADS["C1"].with_(ids="zipf", zipf_s=1.2, opt="adagrad")
+    cfg = O.config_from_workload(wl)
+    bt = synthgen.make_batch(wl, batch=256)
+    layer = _layer(wl, 256, bt.nnz)
+    ora = O.OracleEmbedding(cfg)
+    try:
+        out = np.empty((256, wl.num_slots, wl.dim), np.float32)
+        layer.lookup_host(bt.ids, bt.offsets, 256, bt.nnz, out)
+        layer.backward_update_host(bt.dy, 0.05)
+        (Yo,) = ora.lookup([(bt.ids, bt.offsets, 256)])
+        ora.backward_update([bt.dy], 0.05)
+        _check_close(out, Yo, "Y host path")
+        g = _touched_rows(cfg, bt)
+        w, a = _read_global(layer, cfg, g)
+        _check_close(w, ora.rows(g)[0], "w host path")
+    finally:
+        layer.close()
