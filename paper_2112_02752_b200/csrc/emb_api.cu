@@ -74,13 +74,19 @@ struct emb_ctx {
 
   // ---- workspace
   std::vector<void *> allocs;
-  uint32_t *key_csr = nullptr, *bag_of = nullptr, *k0 = nullptr, *v0 = nullptr, *k1 = nullptr, *v1 = nullptr;
+  uint32_t *key_csr = nullptr, *drow = nullptr, *k0 = nullptr, *v0 = nullptr, *k1 = nullptr, *v1 = nullptr;
   int32_t *blen = nullptr;
   SortWorkspace sws{};
   double *partials = nullptr;
   uint32_t *tickets = nullptr;
-  uint32_t *useg = nullptr, *ukey = nullptr, *ustart = nullptr, *u_count = nullptr, *uniq_status = nullptr,
-           *uniq_counter = nullptr;
+  uint32_t *useg = nullptr, *ukey = nullptr, *ustart = nullptr, *uend = nullptr, *u_count = nullptr,
+           *uniq_status = nullptr, *uniq_counter = nullptr;
+  // world == 1 per-table sort (segsort.cu): table groups of the slot-major CSR
+  bool segsort_ok = false;
+  int32_t G = 0;
+  int32_t *d_gslot = nullptr;
+  uint64_t *d_gbase = nullptr;
+  uint32_t *d_grows = nullptr, *d_gbits = nullptr;
   uint32_t *err_dev = nullptr;
   uint32_t *err_host = nullptr;      // pinned, mapped
   uint32_t *err_host_dev = nullptr;  // device alias of err_host
@@ -93,6 +99,8 @@ struct emb_ctx {
   float *gloc = nullptr;             // [max_ids][D]
   float *grecv = nullptr;            // [recv_cap][D]
   uint32_t *ok0 = nullptr, *ov0 = nullptr, *ok1 = nullptr, *ov1 = nullptr;  // owner sort buffers
+  uint32_t *ouseg = nullptr, *oukey = nullptr, *oustart = nullptr, *ouend = nullptr, *ou_count = nullptr,
+           *ouniq_status = nullptr, *ouniq_counter = nullptr;  // owner-side dedup of the received keys
   int64_t *d_counts = nullptr;       // [2][EMB_MAX_WORLD] send, recv
   int64_t *h_counts = nullptr;       // pinned [2*EMB_MAX_WORLD + 1]
   int64_t recv_cap = 0;
@@ -302,10 +310,11 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   const int W = h->world;
   h->recv_cap = W > 1 ? (int64_t)W * N : N;
   const int64_t grad_n = std::max<int64_t>(N, h->recv_cap);
-  const int64_t nchunks = (grad_n + 31) / 32 + 1;
+  const int64_t nticket = grad_n + 1;
+  const int64_t nwarps_max = grad_max_warps(h->device);
   bool bad = false;
   bad |= dalloc(h, &h->key_csr, N) != cudaSuccess;
-  bad |= dalloc(h, &h->bag_of, N) != cudaSuccess;
+  bad |= dalloc(h, &h->drow, N) != cudaSuccess;
   bad |= dalloc(h, &h->k0, N) != cudaSuccess;
   bad |= dalloc(h, &h->v0, N) != cudaSuccess;
   bad |= dalloc(h, &h->k1, N) != cudaSuccess;
@@ -315,11 +324,12 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   uint32_t *sort_words = nullptr;
   const size_t sww = sort_workspace_words(sort_n);
   bad |= dalloc(h, &sort_words, sww) != cudaSuccess;
-  bad |= dalloc(h, &h->partials, (size_t)2 * nchunks * h->D) != cudaSuccess;
-  bad |= dalloc(h, &h->tickets, nchunks) != cudaSuccess;
+  bad |= dalloc(h, &h->partials, (size_t)2 * nwarps_max * h->D) != cudaSuccess;
+  bad |= dalloc(h, &h->tickets, nticket) != cudaSuccess;
   bad |= dalloc(h, &h->useg, sort_n) != cudaSuccess;
   bad |= dalloc(h, &h->ukey, sort_n) != cudaSuccess;
   bad |= dalloc(h, &h->ustart, sort_n + 1) != cudaSuccess;
+  bad |= dalloc(h, &h->uend, sort_n + 1) != cudaSuccess;
   bad |= dalloc(h, &h->u_count, 2) != cudaSuccess;
   bad |= dalloc(h, &h->uniq_status, unique_status_words(sort_n)) != cudaSuccess;
   bad |= dalloc(h, &h->uniq_counter, 1) != cudaSuccess;
@@ -337,6 +347,13 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
     bad |= dalloc(h, &h->ok1, h->recv_cap) != cudaSuccess;
     bad |= dalloc(h, &h->ov1, h->recv_cap) != cudaSuccess;
     bad |= dalloc(h, &h->d_counts, 2 * EMB_MAX_WORLD) != cudaSuccess;
+    bad |= dalloc(h, &h->ouseg, h->recv_cap) != cudaSuccess;
+    bad |= dalloc(h, &h->oukey, h->recv_cap) != cudaSuccess;
+    bad |= dalloc(h, &h->oustart, h->recv_cap + 1) != cudaSuccess;
+    bad |= dalloc(h, &h->ouend, h->recv_cap + 1) != cudaSuccess;
+    bad |= dalloc(h, &h->ou_count, 2) != cudaSuccess;
+    bad |= dalloc(h, &h->ouniq_status, unique_status_words(h->recv_cap)) != cudaSuccess;
+    bad |= dalloc(h, &h->ouniq_counter, 1) != cudaSuccess;
   }
   if (bad) return fail(h, EMB_ERR_NOMEM, "cannot allocate the step workspace");
   h->sws.hist = sort_words;
@@ -344,7 +361,36 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   h->sws.status = sort_words + 4 * 256 + 4;
   h->sws.max_tiles = (sort_n + 4095) / 4096 + 1;
   h->sws.err = h->err_dev;
-  CUDA_TRY(h, cudaMemset(h->tickets, 0, sizeof(uint32_t) * nchunks));
+  CUDA_TRY(h, cudaMemset(h->tickets, 0, sizeof(uint32_t) * nticket));
+  // table groups of the slot-major CSR (segsort fast path needs a non-decreasing slot_table)
+  if (W == 1) {
+    h->segsort_ok = true;
+    for (int s = 1; s < h->S; ++s)
+      if (h->slot_table[s] < h->slot_table[s - 1]) h->segsort_ok = false;
+    if (h->segsort_ok) {
+      std::vector<int32_t> gslot;
+      std::vector<uint64_t> gbase;
+      std::vector<uint32_t> grows, gbits;
+      for (int s = 0; s < h->S; ++s) {
+        if (s == 0 || h->slot_table[s] != h->slot_table[s - 1]) {
+          const int t = h->slot_table[s];
+          gslot.push_back(s);
+          gbase.push_back(h->base[t]);
+          grows.push_back((uint32_t)h->rows[t]);
+          gbits.push_back(bits_for((uint64_t)h->rows[t]));
+        }
+      }
+      gslot.push_back(h->S);
+      h->G = (int32_t)gbase.size();
+      if (dalloc(h, &h->d_gslot, gslot.size()) || dalloc(h, &h->d_gbase, h->G) || dalloc(h, &h->d_grows, h->G) ||
+          dalloc(h, &h->d_gbits, h->G))
+        return fail(h, EMB_ERR_NOMEM, "alloc groups");
+      CUDA_TRY(h, cudaMemcpy(h->d_gslot, gslot.data(), sizeof(int32_t) * gslot.size(), cudaMemcpyHostToDevice));
+      CUDA_TRY(h, cudaMemcpy(h->d_gbase, gbase.data(), sizeof(uint64_t) * h->G, cudaMemcpyHostToDevice));
+      CUDA_TRY(h, cudaMemcpy(h->d_grows, grows.data(), sizeof(uint32_t) * h->G, cudaMemcpyHostToDevice));
+      CUDA_TRY(h, cudaMemcpy(h->d_gbits, gbits.data(), sizeof(uint32_t) * h->G, cudaMemcpyHostToDevice));
+    }
+  }
   CUDA_TRY(h, cudaMemset(h->err_dev, 0, sizeof(uint32_t)));
   CUDA_TRY(h, cudaMemset(h->u_count, 0, 2 * sizeof(uint32_t)));
   void *hp = nullptr;
@@ -441,7 +487,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   ka.rows = h->d_rows;
   ka.ks = h->ks;
   ka.key = h->key_csr;
-  ka.bag_of = h->bag_of;
+  ka.drow = h->drow;
   ka.blen = h->blen;
   ka.err = h->err_dev;
   if (batch > 0) LAUNCH(h, KID_KEYS, st, launch_keys(ka, st));
@@ -462,11 +508,32 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     // fork: the sort runs on the side stream while the pool streams rows on the caller stream
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-    int nl = 0;
-    cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz, h->ks.key_bits,
-                                     h->side, &h->skey, &h->spay, &nl, prof_hook, h);
-    if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
-    h->launches += nl;
+    if (h->segsort_ok) {
+      SegSortArgs sa{};
+      sa.key_csr = h->key_csr;
+      sa.offsets = offsets;
+      sa.nnz = nnz;
+      sa.batch = batch;
+      sa.gslot = h->d_gslot;
+      sa.gbase = h->d_gbase;
+      sa.grows = h->d_grows;
+      sa.gbits = h->d_gbits;
+      sa.skey = h->k0;
+      sa.spay = h->v0;
+      sa.scratch_k = h->k1;
+      sa.scratch_a = h->v1;
+      sa.scratch_b = h->useg;  // free during the forward (the unique arrays are only filled on demand)
+      sa.err = h->err_dev;
+      h->skey = h->k0;
+      h->spay = h->v0;
+      if (batch > 0) LAUNCH(h, KID_SORT_PASS, h->side, launch_segsort(sa, h->G, h->side));
+    } else {
+      int nl = 0;
+      cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz,
+                                       h->ks.key_bits, h->side, &h->skey, &h->spay, &nl, prof_hook, h);
+      if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+      h->launches += nl;
+    }
     pa.rows_src = h->w;
     pa.nrows_src = h->rows_local;
     pa.row_idx = nullptr;
@@ -485,10 +552,10 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
                                    &h->skey, &h->spay, &nl, prof_hook, h);
   if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
   h->launches += nl;
-  UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->u_count, h->uniq_status, h->uniq_counter};
+  UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter};
   LAUNCH(h, KID_UNIQUE, st, launch_unique(ua, st));
   LAUNCH(h, KID_ROUTE, st, launch_owner_counts(h->ukey, h->u_count, W, h->ks.lbits, h->d_counts, st));
-  LAUNCH(h, KID_ROUTE, st, launch_scatter_inverse(h->spay, h->useg, nnz, h->inv, h->u_count, h->ustart, st));
+  LAUNCH(h, KID_ROUTE, st, launch_scatter_inverse(h->skey, h->spay, h->useg, nnz, h->inv, st));
   LAUNCH(h, KID_ROUTE, st, launch_local_of_unique(h->ukey, h->u_count, nnz, h->lmask, h->send_keys, st));
   // X0: per-peer counts
   {
@@ -524,7 +591,14 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   e = radix_sort_pairs(h->sws, h->recv_keys, nullptr, h->ok0, h->ov0, h->ok1, h->ov1, h->n_recv, h->owner_key_bits,
                        h->side, &h->okey, &h->opay, &nl, prof_hook, h);
   if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("owner sort: ") + cudaGetErrorString(e));
-  // note: the owner sort shares the sort workspace with nothing else in flight on the main stream
+  h->launches += nl;
+  {
+    UniqueArgs ua{h->okey,        h->n_recv,   h->ouseg,         h->oukey,        h->oustart,
+                  h->ouend,       h->ou_count, h->ouniq_status, h->ouniq_counter};
+    LAUNCH(h, KID_UNIQUE, h->side, launch_unique(ua, h->side));
+  }
+  // (the owner sort is the only user of the sort workspace while it runs: the requester sort finished
+  // before X1 on the main stream, and the next step's sort waits for the join below)
   // gather requested rows and send them back
   LAUNCH(h, KID_OWNER_GATHER, st, launch_owner_gather(h->w, h->recv_keys, h->n_recv, h->D, h->owner_rows, st));
   es = exchange(h, h->owner_rows, h->recv_counts, h->roff, h->uniq_rows, h->send_counts, h->soff, sizeof(float),
@@ -550,7 +624,7 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
   GradArgs g{};
   g.dim = h->D;
   g.dy = d_out;
-  g.bag_of = h->bag_of;
+  g.drow = h->drow;
   g.blen = mean ? h->blen : nullptr;
   g.batch = h->batch;
   g.num_slots = h->S;
@@ -566,6 +640,9 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
   g.nsrc_occ = h->nnz;
   g.nout = h->U_l;
   g.err = h->err_dev;
+  g.useg = h->useg;
+  g.ustart = h->ustart;
+  g.u_count = h->u_count;
   if (h->world == 1) {
     g.skey = h->skey;
     g.spay = h->spay;
@@ -583,7 +660,6 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
   g.n = h->nnz;
   g.src_mode = 0;
   g.sink_mode = 1;
-  g.useg = h->useg;
   g.out_rows = h->gloc;
   LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
   emb_status_t es = exchange(h, h->gloc, h->send_counts, h->soff, h->grecv, h->recv_counts, h->roff, sizeof(float),
@@ -597,6 +673,9 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
   o.src_mode = 1;
   o.src = h->grecv;
   o.nsrc = h->n_recv;
+  o.useg = h->ouseg;
+  o.ustart = h->oustart;
+  o.u_count = h->ou_count;
   o.blen = nullptr;
   o.sink_mode = 0;
   o.lmask = 0xFFFFFFFFu;
@@ -607,10 +686,10 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
 
 // host-side unique of the last step (runs the GPU dedup kernel if the step did not)
 emb_status_t ensure_unique(emb_ctx *h) {
-  if (h->world > 1) return EMB_OK;
-  if (h->U_l >= 0) return EMB_OK;
+  if (h->world > 1 || h->U_l >= 0) return EMB_OK;
+  // world == 1: the step itself never needs the compacted unique list; build it on demand
   cudaStream_t st = h->last_stream;
-  UniqueArgs ua{h->skey, h->nnz, h->useg, h->ukey, h->ustart, h->u_count, h->uniq_status, h->uniq_counter};
+  UniqueArgs ua{h->skey, h->nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter};
   CUDA_TRY(h, launch_unique(ua, st));
   uint32_t u = 0;
   CUDA_TRY(h, cudaMemcpyAsync(&u, h->u_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -619,15 +698,17 @@ emb_status_t ensure_unique(emb_ctx *h) {
   return EMB_OK;
 }
 
-emb_status_t copy_unique(emb_ctx *h, const uint32_t *skey_dev, const uint32_t *ukey_dev, const uint32_t *ustart_dev,
+emb_status_t copy_unique(emb_ctx *h, const uint32_t *uend_dev, const uint32_t *ukey_dev, const uint32_t *ustart_dev,
                          int64_t U, bool routing_keys, bool owner_local_keys, uint64_t *keys_host,
                          int64_t *counts_host, int64_t cap, int64_t *n_out) {
-  (void)skey_dev;
   if (n_out) *n_out = U;
   if (cap < U) return fail(h, EMB_ERR_INVALID, "capacity smaller than the number of unique keys");
-  std::vector<uint32_t> k(U), s(U + 1);
-  if (U > 0) CUDA_TRY(h, cudaMemcpy(k.data(), ukey_dev, sizeof(uint32_t) * U, cudaMemcpyDeviceToHost));
-  CUDA_TRY(h, cudaMemcpy(s.data(), ustart_dev, sizeof(uint32_t) * (U + 1), cudaMemcpyDeviceToHost));
+  std::vector<uint32_t> k(U), s(U), e(U);
+  if (U > 0) {
+    CUDA_TRY(h, cudaMemcpy(k.data(), ukey_dev, sizeof(uint32_t) * U, cudaMemcpyDeviceToHost));
+    CUDA_TRY(h, cudaMemcpy(s.data(), ustart_dev, sizeof(uint32_t) * U, cudaMemcpyDeviceToHost));
+    CUDA_TRY(h, cudaMemcpy(e.data(), uend_dev, sizeof(uint32_t) * U, cudaMemcpyDeviceToHost));
+  }
   for (int64_t u = 0; u < U; ++u) {
     if (keys_host) {
       uint64_t g;
@@ -640,7 +721,7 @@ emb_status_t copy_unique(emb_ctx *h, const uint32_t *skey_dev, const uint32_t *u
       }
       keys_host[u] = g;
     }
-    if (counts_host) counts_host[u] = (int64_t)s[u + 1] - (int64_t)s[u];
+    if (counts_host) counts_host[u] = (int64_t)e[u] - (int64_t)s[u];
   }
   if (keys_host && !owner_local_keys && h->world > 1) {
     // requester keys are owner-major; report them sorted by global key like the oracle's U
@@ -850,19 +931,9 @@ emb_status_t emb_last_step_info(emb_handle_t h, emb_step_info_t *info) {
       info->send_counts[p] = h->send_counts[p];
       info->recv_counts[p] = h->recv_counts[p];
     }
-    // owner-side unique count (dedup of the sorted received keys)
-    UniqueArgs ua{h->okey, h->n_recv, h->useg, h->ukey, h->ustart, h->u_count + 1, h->uniq_status, h->uniq_counter};
-    if (h->n_recv > 0) {
-      CUDA_TRY(h, launch_unique(ua, h->last_stream));
-      uint32_t u = 0;
-      CUDA_TRY(h, cudaMemcpyAsync(&u, h->u_count + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, h->last_stream));
-      CUDA_TRY(h, cudaStreamSynchronize(h->last_stream));
-      info->unique_owner = u;
-      // restore the requester-side unique arrays that the owner dedup overwrote
-      UniqueArgs ub{h->skey, h->nnz, h->useg, h->ukey, h->ustart, h->u_count, h->uniq_status, h->uniq_counter};
-      CUDA_TRY(h, launch_unique(ub, h->last_stream));
-      CUDA_TRY(h, cudaStreamSynchronize(h->last_stream));
-    }
+    uint32_t u = 0;
+    CUDA_TRY(h, cudaMemcpy(&u, h->ou_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    info->unique_owner = h->n_recv > 0 ? u : 0;
   }
   return EMB_OK;
 }
@@ -875,7 +946,7 @@ emb_status_t emb_last_unique(emb_handle_t h, uint64_t *keys_host, int64_t *count
   if (s != EMB_OK) return s;
   uint32_t U = 0;
   CUDA_TRY(h, cudaMemcpy(&U, h->u_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  return copy_unique(h, h->skey, h->ukey, h->ustart, U, true, false, keys_host, counts_host, cap, n_out);
+  return copy_unique(h, h->uend, h->ukey, h->ustart, U, true, false, keys_host, counts_host, cap, n_out);
 }
 
 emb_status_t emb_last_owner_unique(emb_handle_t h, uint64_t *keys_host, int64_t *counts_host, int64_t cap,
@@ -884,23 +955,9 @@ emb_status_t emb_last_owner_unique(emb_handle_t h, uint64_t *keys_host, int64_t 
   if (h->world == 1) return emb_last_unique(h, keys_host, counts_host, cap, n_out);
   CUDA_TRY(h, cudaSetDevice(h->device));
   if (h->last_stream) CUDA_TRY(h, cudaStreamSynchronize(h->last_stream));
-  uint32_t *useg2 = nullptr, *ukey2 = nullptr, *ust2 = nullptr;
-  const int64_t n = h->n_recv;
-  CUDA_TRY(h, cudaMalloc(&useg2, sizeof(uint32_t) * std::max<int64_t>(n, 1)));
-  CUDA_TRY(h, cudaMalloc(&ukey2, sizeof(uint32_t) * std::max<int64_t>(n, 1)));
-  CUDA_TRY(h, cudaMalloc(&ust2, sizeof(uint32_t) * (n + 1)));
-  UniqueArgs ua{h->okey, n, useg2, ukey2, ust2, h->u_count + 1, h->uniq_status, h->uniq_counter};
-  cudaError_t e = launch_unique(ua, h->last_stream);
   uint32_t U = 0;
-  if (e == cudaSuccess) e = cudaStreamSynchronize(h->last_stream);
-  if (e == cudaSuccess) e = cudaMemcpy(&U, h->u_count + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost);
-  emb_status_t s = EMB_OK;
-  if (e == cudaSuccess) s = copy_unique(h, h->okey, ukey2, ust2, U, false, true, keys_host, counts_host, cap, n_out);
-  cudaFree(useg2);
-  cudaFree(ukey2);
-  cudaFree(ust2);
-  if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("owner unique: ") + cudaGetErrorString(e));
-  return s;
+  if (h->n_recv > 0) CUDA_TRY(h, cudaMemcpy(&U, h->ou_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return copy_unique(h, h->ouend, h->oukey, h->oustart, U, false, true, keys_host, counts_host, cap, n_out);
 }
 
 int64_t emb_rows_local(emb_handle_t h) { return h ? h->rows_local : -1; }

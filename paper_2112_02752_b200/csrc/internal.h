@@ -64,8 +64,8 @@ struct KeysArgs {
   const int64_t *rows;        // device [T]
   KeySpace ks;
   uint32_t *key;     // out [nnz] routing key or EMB_SENTINEL
-  uint32_t *bag_of;  // out [nnz] bag index s*B+b
-  int32_t *blen;     // out [S*B] bag length
+  uint32_t *drow;    // out [nnz] output row index b*S+s of the occurrence's bag (row of Y and dY)
+  int32_t *blen;     // out [B*S] bag length, indexed by output row b*S+s
   uint32_t *err;     // sticky device error word
 };
 cudaError_t launch_keys(const KeysArgs &a, cudaStream_t st);
@@ -112,9 +112,9 @@ struct GradArgs {
   // contribution source: mode 0 = dY rows via bag_of/blen; mode 1 = rows of `src` at index spay
   int32_t src_mode;
   const float *dy;         // [B][S][D]
-  const uint32_t *bag_of;  // [nnz]
-  int64_t nsrc_occ;        // entries of bag_of (bounds guard)
-  const int32_t *blen;     // [S*B] (mean) or nullptr
+  const uint32_t *drow;    // [nnz] dY row index b*S+s per occurrence
+  int64_t nsrc_occ;        // entries of drow (bounds guard)
+  const int32_t *blen;     // [B*S] bag length by dY row (mean) or nullptr
   int32_t batch, num_slots;
   const float *src;        // mode 1
   // sink: mode 0 = optimizer apply on table rows (local row = key & lmask); mode 1 = write fp32 row
@@ -128,19 +128,23 @@ struct GradArgs {
   int64_t nsrc;            // rows of dy (S*B) or src (bounds guard)
   int64_t nout;            // rows of out_rows (bounds guard)
   uint32_t *err;
-  const uint32_t *useg;    // sink mode 1: unique index per sorted position
+  const uint32_t *useg;    // unique index per sorted position (dedup of skey)
+  const uint32_t *ustart;  // segment starts [U+1] (ustart[U] = number of valid positions)
+  const uint32_t *u_count; // device U
   float *out_rows;
-  double *partials;        // [2*nchunks][D]
-  uint32_t *tickets;       // [nchunks], zero on entry, left zero
+  double *partials;        // [2 * max resident warps][D]
+  uint32_t *tickets;       // [>= U], zero on entry, left zero
 };
 cudaError_t launch_grad(const GradArgs &a, cudaStream_t st);
+int64_t grad_max_warps(int dev);
 
-// dedup of sorted keys: useg[p] = unique index of sorted position p, ukey[u], ustart[u] (ustart[U]
-// = number of valid positions), *u_count (device).
+// dedup of sorted keys: useg[p] = unique index of valid sorted position p, ukey[u], segment
+// [ustart[u], uend[u]) (multiplicity = uend - ustart), *u_count = U (device). Sentinel positions
+// (anywhere) are skipped.
 struct UniqueArgs {
   const uint32_t *skey;
   int64_t n;
-  uint32_t *useg, *ukey, *ustart, *u_count;
+  uint32_t *useg, *ukey, *ustart, *uend, *u_count;
   uint32_t *status;  // [tiles] zeroed
   uint32_t *counter; // zeroed
 };
@@ -158,8 +162,25 @@ cudaError_t launch_rows_scatter(float *dst, const int64_t *rows, int64_t n, int3
 // W > 1 helpers
 cudaError_t launch_owner_counts(const uint32_t *ukey, const uint32_t *u_count, int32_t world, uint32_t lbits,
                                 int64_t *send_counts, cudaStream_t st);
-cudaError_t launch_scatter_inverse(const uint32_t *spay, const uint32_t *useg, int64_t n, uint32_t *inv,
-                                   const uint32_t *u_count, const uint32_t *ustart, cudaStream_t st);
+cudaError_t launch_scatter_inverse(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, int64_t n,
+                                   uint32_t *inv, cudaStream_t st);
+
+// per-table stable sort (world == 1 fast path), see segsort.cu
+constexpr int64_t SEG_CAP = 16384;
+struct SegSortArgs {
+  const uint32_t *key_csr;  // [nnz] fused keys in CSR order (EMB_SENTINEL = invalid)
+  const int64_t *offsets;   // [S*B+1]
+  int64_t nnz;
+  int32_t batch;
+  const int32_t *gslot;     // [G+1] slot boundaries of the table groups
+  const uint64_t *gbase;    // [G] first fused key of the group's table
+  const uint32_t *grows;    // [G] rows of the group's table
+  const uint32_t *gbits;    // [G] bits covering [0, rows] (rows = the invalid marker)
+  uint32_t *skey, *spay;    // out [nnz]
+  uint32_t *scratch_k, *scratch_a, *scratch_b;  // [nnz] global buffers for groups above SEG_CAP
+  uint32_t *err;
+};
+cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st);
 cudaError_t launch_local_of_unique(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, uint32_t lmask,
                                    uint32_t *out, cudaStream_t st);
 cudaError_t launch_owner_gather(const float *w, const uint32_t *local, int64_t n, int32_t dim, float *out,

@@ -4,7 +4,8 @@
 // The warp then walks the contiguous id range [start(b0), end(b0+31)) 32 ids at a time (coalesced
 // int64 loads); each id finds its bag by a 5-step shuffle binary search over the lanes' starts, so
 // skewed bag lengths cost no divergence. Outputs per occurrence j: routing key (or EMB_SENTINEL for an
-// invalid id), its bag index; per bag: its length.
+// invalid id) and its output row index b*S+s (the row of Y / dY it pools into); per bag: its length
+// at that same row index.
 #include "common.cuh"
 #include "internal.h"
 
@@ -22,6 +23,7 @@ __global__ void __launch_bounds__(256) k_keys(KeysArgs a) {
   uint32_t bad = 0;
   uint64_t base = 0;
   int64_t rows = 0;
+  uint32_t orow = 0;
   if (inb) {
     st = a.offsets[bag];
     en = a.offsets[bag + 1];
@@ -30,8 +32,10 @@ __global__ void __launch_bounds__(256) k_keys(KeysArgs a) {
     if (bag == nb - 1 && en != a.nnz) bad = EMB_DEVERR_INVALID;
     st = st < 0 ? 0 : (st > a.nnz ? a.nnz : st);
     en = en < st ? st : (en > a.nnz ? a.nnz : en);
-    if (a.blen) a.blen[bag] = (int32_t)(en - st);
-    const int slot = (int)(bag / a.batch);
+    const uint32_t slot = (uint32_t)bag / (uint32_t)a.batch;
+    const uint32_t b = (uint32_t)bag - slot * (uint32_t)a.batch;
+    orow = b * (uint32_t)a.num_slots + slot;
+    if (a.blen) a.blen[orow] = (int32_t)(en - st);
     const int t = a.slot_table[slot];
     base = a.base[t];
     rows = a.rows[t];
@@ -56,6 +60,7 @@ __global__ void __launch_bounds__(256) k_keys(KeysArgs a) {
     const int64_t enl = __shfl_sync(0xffffffffu, en, l);
     const uint64_t basel = __shfl_sync(0xffffffffu, base, l);
     const int64_t rowsl = __shfl_sync(0xffffffffu, rows, l);
+    const uint32_t orowl = __shfl_sync(0xffffffffu, orow, l);
     if (j < hi) {
       const int64_t id = a.ids[j];
       uint32_t rk = EMB_SENTINEL;
@@ -67,7 +72,7 @@ __global__ void __launch_bounds__(256) k_keys(KeysArgs a) {
         rk = route_key(basel + (uint64_t)id, a.ks);
       }
       a.key[j] = rk;
-      a.bag_of[j] = (uint32_t)(b0 + l);
+      a.drow[j] = orowl;
     }
   }
   // one atomic per warp at most

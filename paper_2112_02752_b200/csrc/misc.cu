@@ -18,7 +18,7 @@ constexpr uint32_t UF_AGG = 1u << 30, UF_INC = 2u << 30, UF_MASK = (1u << 30) - 
 
 size_t unique_status_words(int64_t max_n) { return (size_t)((max_n + UQ_TILE - 1) / UQ_TILE + 1) + 1; }
 
-__global__ void __launch_bounds__(UQ_THREADS) k_unique(UniqueArgs a) {
+__global__ void __launch_bounds__(UQ_THREADS) k_unique(const __grid_constant__ UniqueArgs a) {
   __shared__ uint32_t s_tile, s_excl;
   __shared__ uint32_t warp_tot[UQ_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -26,16 +26,16 @@ __global__ void __launch_bounds__(UQ_THREADS) k_unique(UniqueArgs a) {
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t base = tile * UQ_TILE + (int64_t)tid * UQ_ITEMS;
-  uint32_t k[UQ_ITEMS];
-  uint32_t prev = 0;
+  uint32_t k[UQ_ITEMS + 1];
+  uint32_t prev = EMB_SENTINEL;
   if (base > 0 && base - 1 < a.n) prev = a.skey[base - 1];
 #pragma unroll
-  for (int i = 0; i < UQ_ITEMS; ++i) k[i] = (base + i < a.n) ? a.skey[base + i] : EMB_SENTINEL;
+  for (int i = 0; i <= UQ_ITEMS; ++i) k[i] = (base + i < a.n) ? a.skey[base + i] : EMB_SENTINEL;
   uint32_t flags = 0, cnt = 0;
 #pragma unroll
   for (int i = 0; i < UQ_ITEMS; ++i) {
     const uint32_t kp = i == 0 ? prev : k[i - 1];
-    const bool h = k[i] != EMB_SENTINEL && (base + i == 0 || k[i] != kp);
+    const bool h = k[i] != EMB_SENTINEL && k[i] != kp;
     flags |= (uint32_t)h << i;
     cnt += h;
   }
@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(UQ_THREADS) k_unique(UniqueArgs a) {
         *st = UF_INC | (excl + total);
       }
       s_excl = excl;
+      if (tile == (int64_t)gridDim.x - 1) *a.u_count = excl + total;
     }
   }
   __syncthreads();
@@ -75,22 +76,14 @@ __global__ void __launch_bounds__(UQ_THREADS) k_unique(UniqueArgs a) {
 #pragma unroll
   for (int i = 0; i < UQ_ITEMS; ++i) {
     const int64_t p = base + i;
-    if (p >= a.n || k[i] == EMB_SENTINEL) break;
+    if (p >= a.n || k[i] == EMB_SENTINEL) continue;
     if ((flags >> i) & 1u) {
       a.ukey[u] = k[i];
       a.ustart[u] = (uint32_t)p;
       ++u;
     }
     a.useg[p] = u - 1;
-    const uint32_t kn = (i + 1 < UQ_ITEMS) ? k[i + 1] : ((p + 1 < a.n) ? a.skey[p + 1] : EMB_SENTINEL);
-    if (kn == EMB_SENTINEL) {  // last valid position of the whole array
-      a.ustart[u] = (uint32_t)(p + 1);
-      *a.u_count = u;
-    }
-  }
-  if (tile == 0 && tid == 0 && (a.n == 0 || k[0] == EMB_SENTINEL)) {
-    a.ustart[0] = 0;
-    *a.u_count = 0;
+    if (k[i + 1] != k[i]) a.uend[u - 1] = (uint32_t)(p + 1);  // last position of the segment
   }
 }
 
@@ -127,17 +120,17 @@ cudaError_t launch_owner_counts(const uint32_t *ukey, const uint32_t *u_count, i
   return cudaGetLastError();
 }
 
-__global__ void k_scatter_inverse(const uint32_t *spay, const uint32_t *useg, int64_t n, uint32_t *inv,
-                                  const uint32_t *u_count, const uint32_t *ustart) {
+__global__ void k_scatter_inverse(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, int64_t n,
+                                  uint32_t *inv) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const uint32_t nvalid = ustart[*u_count];
-  inv[spay[p]] = (uint32_t)p < nvalid ? useg[p] : EMB_SENTINEL;
+  const uint32_t k = skey[p];
+  inv[spay[p]] = k != EMB_SENTINEL ? useg[p] : EMB_SENTINEL;
 }
-cudaError_t launch_scatter_inverse(const uint32_t *spay, const uint32_t *useg, int64_t n, uint32_t *inv,
-                                   const uint32_t *u_count, const uint32_t *ustart, cudaStream_t st) {
+cudaError_t launch_scatter_inverse(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, int64_t n,
+                                   uint32_t *inv, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  k_scatter_inverse<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(spay, useg, n, inv, u_count, ustart);
+  k_scatter_inverse<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(skey, spay, useg, n, inv);
   return cudaGetLastError();
 }
 

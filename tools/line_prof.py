@@ -1,0 +1,43 @@
+"""Attribute ncu per-SASS-instruction counts / stall samples to source lines via nvdisasm -g."""
+import csv, re, sys
+from collections import defaultdict
+sass_file, func, csv_file = sys.argv[1], sys.argv[2], sys.argv[3]
+lines = open(sass_file).read().splitlines()
+start = None
+for i, l in enumerate(lines):
+    if l.startswith(".text." + func + ":"):
+        start = i
+        break
+off2line = {}
+cur = None
+for l in lines[start + 1:]:
+    if l.startswith(".text.") or l.startswith("//---"):
+        break
+    m = re.search(r'line (\d+)', l)
+    if "## File" in l and m:
+        if "inlined at" not in l:
+            cur = int(m.group(1))
+        continue
+    m = re.match(r'\s*/\*([0-9a-f]{4,})\*/', l)
+    if m:
+        off2line[int(m.group(1), 16)] = cur
+rows = list(csv.reader(open(csv_file)))
+hdr = rows[1]
+ai, ii, ti = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+data = []
+for r in rows[2:]:
+    try:
+        data.append((int(r[ai], 16), float(r[ii] or 0), float(r[ti] or 0)))
+    except (ValueError, IndexError):
+        pass
+base = min(d[0] for d in data)
+agg_i, agg_s = defaultdict(float), defaultdict(float)
+for a, n, s in data:
+    ln = off2line.get(a - base)
+    agg_i[ln] += n
+    agg_s[ln] += s
+ti_, ts_ = sum(agg_i.values()), sum(agg_s.values())
+src = open(sys.argv[4]).read().splitlines() if len(sys.argv) > 4 else None
+for ln in sorted(agg_i, key=lambda k: -agg_i[k])[:30]:
+    txt = src[ln - 1].strip()[:80] if (src and ln) else ""
+    print("L%-5s inst %5.1f%%  stall %5.1f%%  %s" % (ln, 100 * agg_i[ln] / ti_, 100 * agg_s[ln] / ts_, txt))
