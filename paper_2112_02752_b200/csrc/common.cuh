@@ -84,6 +84,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
       : "memory");
 }
 
+// ---- per-thread async copies (cp.async, SASS LDGSTS): 16 B global -> shared, L2 only ------------
+__device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void *src_gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src_gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---- warp helpers -----------------------------------------------------------------------------
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
