@@ -9,7 +9,7 @@
 // entirely in shared memory (keys + two index buffers, 12 B per occurrence, up to SEG_CAP = 16,384
 // occurrences). Each pass counts digits per warp with shared-memory atomics over the warp's
 // contiguous chunk, scans the (digit, warp) counters digit-major across the CTA's 32 warps, then ranks
-// stably with the warp-level multisplit of radix_sort.cu (__match_any_sync per 32-item row) while
+// stably with a warp-level multisplit (peer masks from 8 ballots per 32-item row) while
 // scattering. Larger groups run the same code on global-memory scratch (correct, slower).
 // Invalid occurrences (EMB_SENTINEL) get local key rows[t] and sort to the end of their group.
 #include "common.cuh"
@@ -21,6 +21,18 @@ namespace {
 constexpr int SS_THREADS = 1024;
 constexpr int SS_WARPS = SS_THREADS / 32;
 }  // namespace
+
+// lanes of the warp holding the same 8-bit digit as this lane (8 ballots; cheaper than match.any)
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
+  uint32_t m = __ballot_sync(0xffffffffu, valid);
+  if (!valid) m = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+    m &= ((d >> b) & 1u) ? bb : ~bb;
+  }
+  return m;
+}
 
 size_t segsort_smem_bytes() { return (size_t)SEG_CAP * 12; }
 
@@ -50,10 +62,10 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort(const __grid_constant__ 
     ia = a.scratch_a + lo;
     ib = a.scratch_b + lo;
   }
+#pragma unroll 4
   for (int64_t i = tid; i < n; i += SS_THREADS) {
     const uint32_t k = a.key_csr[lo + i];
     keys[i] = (k == EMB_SENTINEL) ? rows : k - base;
-    ia[i] = (uint32_t)i;
   }
   __syncthreads();
   const int64_t chunk = ((n + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;  // rows of 32 per warp
@@ -100,8 +112,8 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort(const __grid_constant__ 
       const bool valid = p < c_hi;
       const uint32_t item = valid ? (pass == 0 ? (uint32_t)p : ia[p]) : 0u;
       const uint32_t d = valid ? (keys[item] >> shift) & 0xFFu : 0u;
-      const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : (0x100u | lane));
-      const int leader = __ffs(peers) - 1;
+      const uint32_t peers = digit_peers(d, valid);
+      const int leader = valid ? __ffs(peers) - 1 : 0;
       uint32_t basepos = 0;
       if (valid && lane == leader) {
         basepos = cnt[w][d];

@@ -1,0 +1,41 @@
+"""Multi-GPU parity (-m gpu, needs >= 2 GPUs): row-sharded layer over 2 GPUs with NCCL all-to-alls
+inside libemb vs the serial oracle (tests/mgpu_worker.py, one process per GPU via torchrun)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpu():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("case,shard", [("c3", "cyclic"), ("hot", "cyclic"), ("c3", "block")])
+def test_two_gpu_row_sharded_parity(case, shard):
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    from paper_2112_02752_b200 import build
+    build.build()
+    env = dict(os.environ, EMB_MGPU_CASE=case, EMB_MGPU_SHARD=shard)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tests", "mgpu_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
