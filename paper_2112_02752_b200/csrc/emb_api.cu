@@ -83,7 +83,8 @@ struct emb_ctx {
            *uniq_status = nullptr, *uniq_counter = nullptr;
   // world == 1 per-table sort (segsort.cu): table groups of the slot-major CSR
   bool segsort_ok = false;
-  int32_t G = 0;
+  int32_t G = 0, segK = 1;
+  uint32_t *run_k = nullptr, *run_i = nullptr;
   int32_t *d_gslot = nullptr;
   uint64_t *d_gbase = nullptr;
   uint32_t *d_grows = nullptr, *d_gbits = nullptr;
@@ -293,7 +294,13 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   if (dalloc(h, &h->w, row_elems) != cudaSuccess) return fail(h, EMB_ERR_NOMEM, "cannot allocate the table shard");
   if (h->opt == EMB_OPT_ADAGRAD && dalloc(h, &h->a, row_elems) != cudaSuccess)
     return fail(h, EMB_ERR_NOMEM, "cannot allocate the Adagrad state");
-  CUDA_TRY(h, cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  {
+    // the side stream carries the latency-critical sort: highest priority, so its CTAs are scheduled
+    // ahead of the bandwidth-bound pool CTAs as SMs free up
+    int lo_prio = 0, hi_prio = 0;
+    CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi_prio));
+  }
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CUDA_TRY(h, launch_init(h->w, h->a, h->rows_local, h->D, h->seed, h->init_accum, ks, h->rank, h->side));
@@ -382,6 +389,12 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
       }
       gslot.push_back(h->S);
       h->G = (int32_t)gbase.size();
+      // key ranges (CTAs) per group: ~2K occurrences per CTA at the capacity bound; every CTA scans
+      // its whole group, so K stays small
+      const int64_t per = (h->max_ids + h->G - 1) / h->G;
+      h->segK = (int32_t)std::min<int64_t>(16, std::max<int64_t>(1, (per + 2047) / 2048));
+      if (dalloc(h, &h->run_k, h->max_ids) || dalloc(h, &h->run_i, h->max_ids))
+        return fail(h, EMB_ERR_NOMEM, "alloc sort runs");
       if (dalloc(h, &h->d_gslot, gslot.size()) || dalloc(h, &h->d_gbase, h->G) || dalloc(h, &h->d_grows, h->G) ||
           dalloc(h, &h->d_gbits, h->G))
         return fail(h, EMB_ERR_NOMEM, "alloc groups");
@@ -490,7 +503,9 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   ka.drow = h->drow;
   ka.blen = h->blen;
   ka.err = h->err_dev;
-  if (batch > 0) LAUNCH(h, KID_KEYS, st, launch_keys(ka, st));
+  // W == 1 with the per-table sort: pool and sort read the ids themselves (no key kernel)
+  const bool direct = h->world == 1 && h->segsort_ok;
+  if (batch > 0 && !direct) LAUNCH(h, KID_KEYS, st, launch_keys(ka, st));
 
   PoolArgs pa{};
   pa.key = h->key_csr;
@@ -503,6 +518,14 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   pa.out = out;
   pa.err = h->err_dev;
   pa.err_host = h->err_host_dev;
+  if (direct) {
+    pa.ids = ids;
+    pa.slot_table = h->d_slot_table;
+    pa.base = h->d_base;
+    pa.rows = h->d_rows;
+    pa.drow = h->drow;
+    pa.blen = mean ? h->blen : nullptr;
+  }
 
   if (h->world == 1) {
     // fork: the sort runs on the side stream while the pool streams rows on the caller stream
@@ -510,7 +533,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
     if (h->segsort_ok) {
       SegSortArgs sa{};
-      sa.key_csr = h->key_csr;
+      sa.ids = ids;
       sa.offsets = offsets;
       sa.nnz = nnz;
       sa.batch = batch;
@@ -523,6 +546,9 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
       sa.scratch_k = h->k1;
       sa.scratch_a = h->v1;
       sa.scratch_b = h->useg;  // free during the forward (the unique arrays are only filled on demand)
+      sa.run_k = h->run_k;
+      sa.run_i = h->run_i;
+      sa.K = h->segK;
       sa.err = h->err_dev;
       h->skey = h->k0;
       h->spay = h->v0;
@@ -540,6 +566,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
+    if (batch > 0) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
     h->U_l = -1;  // computed on demand
     h->state = 1;
     return EMB_OK;
@@ -610,6 +637,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
   CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
   CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
+  if (batch > 0) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
   h->state = 1;
   return EMB_OK;
 }

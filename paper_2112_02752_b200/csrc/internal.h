@@ -89,7 +89,15 @@ cudaError_t radix_sort_pairs(const SortWorkspace &ws, const uint32_t *kin, const
 
 // W == 1 forward: Y[b][s][:] = pool over bag of table rows, straight from the table.
 struct PoolArgs {
-  const uint32_t *key;     // [nnz] routing keys in CSR order (EMB_SENTINEL = skip)
+  // W == 1 ("direct"): ids != nullptr; the pool validates the CSR and ids itself, computes the row
+  // g = base[t] + id, and writes the per-occurrence dY row index (drow) and bag lengths (blen).
+  const int64_t *ids;      // [nnz] (direct mode) or nullptr
+  const int32_t *slot_table;
+  const uint64_t *base;
+  const int64_t *rows;
+  uint32_t *drow;          // out (direct mode) [nnz]
+  int32_t *blen;           // out (direct mode) [B*S] or nullptr
+  const uint32_t *key;     // [nnz] routing keys in CSR order (EMB_SENTINEL = skip), key mode
   const int64_t *offsets;  // [S*B+1]
   int64_t nnz;
   int32_t batch, num_slots, dim;
@@ -102,6 +110,7 @@ struct PoolArgs {
   uint32_t *err_host;      // mapped pinned host word (may be null)
 };
 cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st);
+cudaError_t launch_publish_err(const uint32_t *err, uint32_t *err_host, cudaStream_t st);
 
 // backward: segment reduce over sorted (key, pay) + sink
 struct GradArgs {
@@ -168,7 +177,7 @@ cudaError_t launch_scatter_inverse(const uint32_t *skey, const uint32_t *spay, c
 // per-table stable sort (world == 1 fast path), see segsort.cu
 constexpr int64_t SEG_CAP = 16384;
 struct SegSortArgs {
-  const uint32_t *key_csr;  // [nnz] fused keys in CSR order (EMB_SENTINEL = invalid)
+  const int64_t *ids;       // [nnz] table-local ids in CSR order (validated here: out of range = invalid)
   const int64_t *offsets;   // [S*B+1]
   int64_t nnz;
   int32_t batch;
@@ -177,7 +186,9 @@ struct SegSortArgs {
   const uint32_t *grows;    // [G] rows of the group's table
   const uint32_t *gbits;    // [G] bits covering [0, rows] (rows = the invalid marker)
   uint32_t *skey, *spay;    // out [nnz]
-  uint32_t *scratch_k, *scratch_a, *scratch_b;  // [nnz] global buffers for groups above SEG_CAP
+  uint32_t *scratch_k, *scratch_a, *scratch_b;  // [nnz] global buffers for chunks above the smem cap
+  uint32_t *run_k, *run_i;  // [nnz] sorted runs (local key, chunk-relative index)
+  int32_t K;                // chunks (CTAs) per group
   uint32_t *err;
 };
 cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st);

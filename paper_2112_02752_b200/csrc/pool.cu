@@ -23,10 +23,20 @@ namespace {
 constexpr int POOL_THREADS = 256;
 }  // namespace
 
-__device__ __forceinline__ uint32_t pool_row_of(const PoolArgs &a, int64_t j) {
+// row of occurrence j. Key mode: from the routing key (W > 1: row = inverse[j]). Direct mode (W == 1):
+// g = base[t] + id validated here (R4), and the occurrence's dY row index recorded for the backward.
+__device__ __forceinline__ uint32_t pool_row_of(const PoolArgs &a, int64_t j, uint32_t slot, uint32_t orow) {
   uint32_t row = EMB_SENTINEL;
-  const uint32_t k = a.key[j];
-  if (k != EMB_SENTINEL) row = a.row_idx ? a.row_idx[j] : k;
+  if (a.ids) {
+    const int t = a.slot_table[slot];
+    const int64_t id = a.ids[j];
+    if (id >= 0 && id < a.rows[t]) row = (uint32_t)(a.base[t] + (uint64_t)id);
+    else atomicOr(a.err, EMB_DEVERR_RANGE);
+    a.drow[j] = orow;
+  } else {
+    const uint32_t k = a.key[j];
+    if (k != EMB_SENTINEL) row = a.row_idx ? a.row_idx[j] : k;
+  }
   if (row != EMB_SENTINEL && (int64_t)row >= a.nrows_src) {
     atomicOr(a.err, EMB_DEVERR_INTERNAL);
     row = EMB_SENTINEL;
@@ -37,7 +47,7 @@ __device__ __forceinline__ uint32_t pool_row_of(const PoolArgs &a, int64_t j) {
 // general tile: flattened walk over the occurrences [lo, hi) of the tile's bags, fp64 in order
 template <int CPL>
 __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, int64_t hi, int64_t my_end,
-                                               uint32_t my_orow, int nbt) {
+                                               uint32_t my_orow, uint32_t my_slot, int nbt) {
   constexpr int RCH = 32 / CPL;
   const int lane = threadIdx.x & 31;
   const int D = a.dim;
@@ -67,13 +77,26 @@ __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, in
     cst = cend;
     cend = __shfl_sync(0xffffffffu, my_end, cb < 32 ? cb : 31);
   };
+  // row of occurrence j (lane-parallel): its bag = the first bag whose end is > j
+  auto occ_row = [&](int64_t j) -> uint32_t {
+    int l = 0;
+#pragma unroll
+    for (int step = 16; step; step >>= 1) {
+      const int64_t e = __shfl_sync(0xffffffffu, my_end, l + step - 1);
+      if (l + step - 1 < nbt && e <= j) l += step;
+    }
+    const uint32_t sl = __shfl_sync(0xffffffffu, my_slot, l < 32 ? l : 31);
+    const uint32_t orw = __shfl_sync(0xffffffffu, my_orow, l < 32 ? l : 31);
+    const bool ok = (lane < RCH) && j < hi;
+    return ok ? pool_row_of(a, j, sl, orw) : EMB_SENTINEL;
+  };
   // close leading empty bags
   while (cb < nbt && cend <= lo) flush();
-  uint32_t nrow = (lo + lane < hi && lane < RCH) ? pool_row_of(a, lo + lane) : EMB_SENTINEL;
+  uint32_t nrow = occ_row(lo + lane);
   for (int64_t j0 = lo; j0 < hi; j0 += RCH) {
     const uint32_t row = nrow;
     const int64_t jn = j0 + RCH;
-    nrow = (jn + lane < hi && lane < RCH) ? pool_row_of(a, jn + lane) : EMB_SENTINEL;  // prefetch
+    nrow = occ_row(jn + lane);  // prefetch
     VecF<CPL> v[RCH];
 #pragma unroll
     for (int r = 0; r < RCH; ++r) {
@@ -108,10 +131,6 @@ __global__ void __launch_bounds__(POOL_THREADS, 3) k_pool(const __grid_constant_
   const int64_t ntiles = (nb + 31) / 32;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  if (gw == 0 && lane == 0 && a.err_host) {
-    // publish the sticky error word of this step's key kernel (it ran before us on the stream)
-    *(volatile uint32_t *)a.err_host = *(volatile const uint32_t *)a.err;
-  }
   for (int64_t tile = gw; tile < ntiles; tile += nwarps) {
     const int64_t b0 = tile * 32;
     const int nbt = (int)((nb - b0) < 32 ? (nb - b0) : 32);
@@ -122,19 +141,26 @@ __global__ void __launch_bounds__(POOL_THREADS, 3) k_pool(const __grid_constant_
       off = a.offsets[bag];
       offn = a.offsets[bag + 1];
     }
+    if (a.ids && inb) {  // direct mode validates the CSR (the key kernel does it in key mode)
+      bool bad = off < 0 || offn < off || offn > a.nnz;
+      if (bag == 0 && off != 0) bad = true;
+      if ((int64_t)bag == nb - 1 && offn != a.nnz) bad = true;
+      if (bad) atomicOr(a.err, EMB_DEVERR_INVALID);
+    }
     off = off < 0 ? 0 : (off > a.nnz ? a.nnz : off);
     offn = offn < off ? off : (offn > a.nnz ? a.nnz : offn);
     const int len = (int)(offn - off);
     const uint32_t s = bag / B;
     const uint32_t orow = (bag - s * B) * S + s;
+    if (a.ids && a.blen && inb) a.blen[orow] = len;
     if (__any_sync(0xffffffffu, len > 1)) {
       const int64_t lo = __shfl_sync(0xffffffffu, off, 0);
       const int64_t hi = __shfl_sync(0xffffffffu, offn, nbt - 1);
-      pool_tile_general<CPL>(a, lo, hi, offn, orow, nbt);
+      pool_tile_general<CPL>(a, lo, hi, offn, orow, s, nbt);
       continue;
     }
     // single-id bags: copy the row (exact)
-    const uint32_t row = (len == 1) ? pool_row_of(a, off) : EMB_SENTINEL;
+    const uint32_t row = (len == 1) ? pool_row_of(a, off, s, orow) : EMB_SENTINEL;
 #pragma unroll
     for (int c0 = 0; c0 < 32; c0 += RCH) {
       if (c0 >= nbt) break;
@@ -160,6 +186,15 @@ static cudaError_t launch_pool_t(const PoolArgs &a, int64_t ntiles, cudaStream_t
   // they are ready and the pool fills the rest
   const int64_t blocks = (ntiles * 32 + POOL_THREADS - 1) / POOL_THREADS;
   k_pool<CPL><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// copy the sticky device error word to the mapped pinned host word (end of every lookup)
+__global__ void k_publish_err(const uint32_t *err, uint32_t *err_host) {
+  *(volatile uint32_t *)err_host = *(volatile const uint32_t *)err;
+}
+cudaError_t launch_publish_err(const uint32_t *err, uint32_t *err_host, cudaStream_t st) {
+  k_publish_err<<<1, 1, 0, st>>>(err, err_host);
   return cudaGetLastError();
 }
 

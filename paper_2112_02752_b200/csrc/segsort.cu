@@ -3,26 +3,35 @@
 //
 // When slot_table is non-decreasing (true for every BASELINE config: C1/C4 share one table, C2/C3/C5
 // map slot s -> table s), the slot-major CSR is already grouped by table and the table groups appear
-// in fused-key order, so sorting the whole array is the same as sorting each group in place. One
-// CTA per group sorts (local id = key - base[t], payload = occurrence index) with a stable LSD radix
-// sort on the group's own key bits (ceil(log2(rows[t]+1)): 24 bits = 3 passes for a 10M-row table)
-// entirely in shared memory (keys + two index buffers, 12 B per occurrence, up to SEG_CAP = 16,384
-// occurrences). Each pass counts digits per warp with shared-memory atomics over the warp's
-// contiguous chunk, scans the (digit, warp) counters digit-major across the CTA's 32 warps, then ranks
-// stably with a warp-level multisplit (peer masks from 8 ballots per 32-item row) while
-// scattering. Larger groups run the same code on global-memory scratch (correct, slower).
-// Invalid occurrences (EMB_SENTINEL) get local key rows[t] and sort to the end of their group.
+// in fused-key order, so sorting the whole array is the same as sorting each group in place.
+//
+// One kernel, K CTAs per table group (v3; v1 = one CTA per group, issue-bound on 26 of 148 SMs; v2 =
+// chunk sorts + a K-way merge by ranking, search-bound):
+//  * CTA (g, b) owns the b-th of K equal ranges of the table's local-id space (bucket(local) =
+//    (local * mul) >> 32, monotone, mul = floor(2^32 K / (rows + 1))). Each warp scans a contiguous
+//    1/16 of the group's keys twice: once to count its items below / inside the range (ballots), then
+//    -- after a block scan of the per-warp counts -- to compact the range's items into shared memory
+//    in occurrence order. The range's output offset is the number of group items in lower ranges.
+//  * the compacted items (local id, occurrence index) are sorted with a stable LSD radix sort on the
+//    group's key bits (24 bits = 3 passes of 8 for a 10M-row table): per pass, per-warp digit counts
+//    (shared-memory atomics over the warp's contiguous sub-chunk), a digit-major scan of the
+//    (digit, warp) counters, then a stable scatter ranked by a warp multisplit (peer masks from 8
+//    ballots per 32-item row);
+//  * items are written straight to their final sorted positions: no merge.
+// Ranges above SEG_CHUNK_CAP items run the same code on global scratch (correct, slower). Invalid
+// occurrences (EMB_SENTINEL) get local key rows[t] and sort to the end of their group.
 #include "common.cuh"
 #include "internal.h"
 
 namespace emb {
 
 namespace {
-constexpr int SS_THREADS = 1024;
+constexpr int SS_THREADS = 512;
 constexpr int SS_WARPS = SS_THREADS / 32;
+constexpr uint32_t SEG_CHUNK_CAP = 8192;  // items per range sorted in shared memory (128 KB)
 }  // namespace
 
-// lanes of the warp holding the same 8-bit digit as this lane (8 ballots; cheaper than match.any)
+// lanes of the warp holding the same 8-bit digit as this lane (8 ballots)
 __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
   uint32_t m = __ballot_sync(0xffffffffu, valid);
   if (!valid) m = 0;
@@ -34,57 +43,108 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
   return m;
 }
 
-size_t segsort_smem_bytes() { return (size_t)SEG_CAP * 12; }
-
-__global__ void __launch_bounds__(SS_THREADS) k_segsort(const __grid_constant__ SegSortArgs a) {
+__device__ __forceinline__ void group_bounds(const SegSortArgs &a, int g, int64_t &lo, int64_t &hi) {
+  const int64_t B = a.batch;
+  lo = a.offsets[(int64_t)a.gslot[g] * B];
+  hi = a.offsets[(int64_t)a.gslot[g + 1] * B];
+  lo = lo < 0 ? 0 : (lo > a.nnz ? a.nnz : lo);
+  hi = hi < lo ? lo : (hi > a.nnz ? a.nnz : hi);
+}
+__global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_constant__ SegSortArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ uint32_t cnt[SS_WARPS][256];
   __shared__ uint32_t part[SS_THREADS / 32];
+  __shared__ uint32_t wbelow[SS_WARPS], wmine[SS_WARPS];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int g = blockIdx.x;
-  const int64_t B = a.batch;
-  int64_t lo = a.offsets[(int64_t)a.gslot[g] * B];
-  int64_t hi = a.offsets[(int64_t)a.gslot[g + 1] * B];
-  lo = lo < 0 ? 0 : (lo > a.nnz ? a.nnz : lo);
-  hi = hi < lo ? lo : (hi > a.nnz ? a.nnz : hi);
-  const int64_t n = hi - lo;
-  if (n == 0) return;
+  const int K = a.K;
+  const int g = blockIdx.x / K, bkt = blockIdx.x % K;
+  int64_t glo, ghi;
+  group_bounds(a, g, glo, ghi);
+  const uint32_t ng = (uint32_t)(ghi - glo);
+  if (ng == 0) return;
   const uint32_t base = (uint32_t)a.gbase[g];
   const uint32_t rows = a.grows[g];
   const uint32_t bits = a.gbits[g];
+  const uint64_t mul = ((uint64_t)K << 32) / ((uint64_t)rows + 1u);
+  // table-local id; invalid ids (R4) become `rows` and sort to the end of the group
+  auto local_of = [&](int64_t id) { return (id >= 0 && id < (int64_t)rows) ? (uint32_t)id : rows; };
+  auto bucket_of = [&](uint32_t lk) {
+    const uint32_t b = (uint32_t)(((uint64_t)lk * mul) >> 32);
+    return b < (uint32_t)K ? b : (uint32_t)K - 1u;
+  };
+  // ---- 1. count: items below / inside this range, per warp over a contiguous 1/16 of the group
+  const uint32_t span = ((ng + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;
+  const uint32_t s_lo = w * span, s_hi = min(ng, s_lo + span);
+  uint32_t below = 0, mine = 0;
+  for (uint32_t r0 = s_lo; r0 < s_hi; r0 += 32) {
+    const uint32_t i = r0 + lane;
+    uint32_t bb = 0xFFFFFFFFu;
+    if (i < s_hi) bb = bucket_of(local_of(a.ids[glo + i]));
+    below += __popc(__ballot_sync(0xffffffffu, bb < (uint32_t)bkt));
+    mine += __popc(__ballot_sync(0xffffffffu, bb == (uint32_t)bkt));
+  }
+  if (lane == 0) {
+    wbelow[w] = below;
+    wmine[w] = mine;
+  }
+  __syncthreads();
+  uint32_t out_lo = 0, my_start = 0, n = 0;
+  for (int q = 0; q < SS_WARPS; ++q) {
+    out_lo += wbelow[q];
+    if (q < w) my_start += wmine[q];
+    n += wmine[q];
+  }
+  if (n == 0) return;
   uint32_t *keys, *ia, *ib;
-  if (n <= SEG_CAP) {
+  if (n <= SEG_CHUNK_CAP) {
     keys = sm;
     ia = sm + n;
     ib = sm + 2 * n;
-  } else {
-    keys = a.scratch_k + lo;
-    ia = a.scratch_a + lo;
-    ib = a.scratch_b + lo;
+  } else {  // oversized range: global scratch at the range's own output slice
+    keys = a.scratch_k + glo + out_lo;
+    ia = a.scratch_a + glo + out_lo;
+    ib = a.scratch_b + glo + out_lo;
   }
-#pragma unroll 4
-  for (int64_t i = tid; i < n; i += SS_THREADS) {
-    const uint32_t k = a.key_csr[lo + i];
-    keys[i] = (k == EMB_SENTINEL) ? rows : k - base;
+  // ---- 2. compact the range's items in occurrence order: keys[] = local id, ia[] = group index
+  {
+    uint32_t cur = my_start;
+    for (uint32_t r0 = s_lo; r0 < s_hi; r0 += 32) {
+      const uint32_t i = r0 + lane;
+      uint32_t lk = 0;
+      bool in = false;
+      if (i < s_hi) {
+        lk = local_of(a.ids[glo + i]);
+        in = bucket_of(lk) == (uint32_t)bkt;
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const uint32_t d = cur + __popc(m & lanemask_lt());
+        keys[d] = lk;
+        ia[d] = i;
+      }
+      cur += __popc(m);
+    }
   }
   __syncthreads();
-  const int64_t chunk = ((n + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;  // rows of 32 per warp
-  const int64_t c_lo = (int64_t)w * chunk;
-  const int64_t c_hi = (c_lo + chunk < n) ? c_lo + chunk : n;
+  // ---- 3. stable LSD radix sort of the n compacted items (ia holds the payload, permuted by value)
+  const uint32_t chunk = ((n + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;  // rows of 32 per warp
+  const uint32_t c_lo = w * chunk;
+  const uint32_t c_hi = min(n, c_lo + chunk);
   const int npass = (int)((bits + 7) / 8);
+  // sort item ordinals 0..n-1 (ping-pong pa/pb); keys[] and ia[] stay in place
+  uint32_t *pa = ib;
+  uint32_t *pb = (n <= SEG_CHUNK_CAP) ? sm + 3 * n : a.run_k + glo + out_lo;
   for (int pass = 0; pass < npass; ++pass) {
     const int shift = 8 * pass;
     for (int d = lane; d < 256; d += 32) cnt[w][d] = 0;
     __syncwarp();
-    // 1. per-warp digit counts over the warp's contiguous chunk (shared-memory atomics)
-    for (int64_t p = c_lo + lane; p < c_hi; p += 32) {
-      const uint32_t item = pass == 0 ? (uint32_t)p : ia[p];
+    for (uint32_t p = c_lo + lane; p < c_hi; p += 32) {
+      const uint32_t item = pass == 0 ? p : pa[p];
       atomicAdd(&cnt[w][(keys[item] >> shift) & 0xFFu], 1u);
     }
     __syncthreads();
-    // 2. digit-major exclusive scan over (digit, warp): thread t owns digit t/4, warps (t&3)*8 .. +7
     {
-      const int d = tid >> 2, w0 = (tid & 3) * 8;
+      const int d = tid >> 1, w0 = (tid & 1) * 8;
       uint32_t s = 0;
 #pragma unroll
       for (int q = 0; q < 8; ++q) s += cnt[w0 + q][d];
@@ -100,17 +160,16 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort(const __grid_constant__ 
       uint32_t run = part[w] + incl - s;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const uint32_t c = cnt[w0 + q][d];
+        const uint32_t cc = cnt[w0 + q][d];
         cnt[w0 + q][d] = run;
-        run += c;
+        run += cc;
       }
     }
     __syncthreads();
-    // 3. stable scatter: same walk, running per-warp digit cursors
-    for (int64_t r0 = c_lo; r0 < c_hi; r0 += 32) {
-      const int64_t p = r0 + lane;
+    for (uint32_t r0 = c_lo; r0 < c_hi; r0 += 32) {
+      const uint32_t p = r0 + lane;
       const bool valid = p < c_hi;
-      const uint32_t item = valid ? (pass == 0 ? (uint32_t)p : ia[p]) : 0u;
+      const uint32_t item = valid ? (pass == 0 ? p : pa[p]) : 0u;
       const uint32_t d = valid ? (keys[item] >> shift) & 0xFFu : 0u;
       const uint32_t peers = digit_peers(d, valid);
       const int leader = valid ? __ffs(peers) - 1 : 0;
@@ -122,34 +181,37 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort(const __grid_constant__ 
       basepos = __shfl_sync(0xffffffffu, basepos, leader);
       if (valid) {
         const uint32_t dst = basepos + __popc(peers & lanemask_lt());
-        if (dst < (uint64_t)n) ib[dst] = item;
+        if (dst < n) pb[dst] = item;
         else atomicOr(a.err, EMB_DEVERR_INTERNAL);
       }
       __syncwarp();
     }
     __syncthreads();
-    uint32_t *t = ia;
-    ia = ib;
-    ib = t;
+    uint32_t *t = pa;
+    pa = pb;
+    pb = t;
   }
-  for (int64_t i = tid; i < n; i += SS_THREADS) {
-    const uint32_t item = ia[i];
+  // ---- 4. final positions: group offset of the range + rank
+  for (uint32_t i = tid; i < n; i += SS_THREADS) {
+    const uint32_t item = npass > 0 ? pa[i] : i;
     const uint32_t lk = keys[item];
-    a.skey[lo + i] = (lk >= rows) ? EMB_SENTINEL : base + lk;
-    a.spay[lo + i] = (uint32_t)(lo + item);
+    a.skey[glo + out_lo + i] = (lk >= rows) ? EMB_SENTINEL : base + lk;
+    a.spay[glo + out_lo + i] = (uint32_t)(glo + ia[item]);
   }
 }
+
+size_t segsort_smem_bytes() { return (size_t)SEG_CHUNK_CAP * 16; }
 
 cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st) {
   if (groups <= 0 || a.nnz <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_segsort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_segsort_range, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)segsort_smem_bytes());
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_segsort<<<groups, SS_THREADS, segsort_smem_bytes(), st>>>(a);
+  k_segsort_range<<<groups * a.K, SS_THREADS, segsort_smem_bytes(), st>>>(a);
   return cudaGetLastError();
 }
 
