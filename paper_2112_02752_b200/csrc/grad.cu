@@ -72,31 +72,36 @@ __device__ __forceinline__ void stg_frag(float *p, const VecF<CPL> &v) {
     asm volatile("st.global.v2.f32 [%0], {%1,%2};" ::"l"(p + c), "f"(v.v[c]), "f"(v.v[c + 1]) : "memory");
 }
 
-// optimizer update (MODE 0/1) of one lane's row fragment, w / a already in registers
+// optimizer constants, converted once per kernel
+struct OptConst {
+  double lr;
+  float lrf, epsf;
+};
+__device__ __forceinline__ OptConst opt_const(const GradArgs &a) { return {a.lr, (float)a.lr, (float)a.eps}; }
+
+// optimizer update (MODE 0/1) of one lane's row fragment, w / a already in registers; D = row width
+// (compile-time when DC != 0)
 template <int CPL, int MODE>
-__device__ __forceinline__ void apply_frag(const GradArgs &a, const double (&acc)[CPL], const VecF<CPL> &wv,
-                                           const VecF<CPL> &av, uint32_t lrow, int col) {
-  float *wg = a.w + (size_t)lrow * a.dim + col;
+__device__ __forceinline__ void apply_frag(const GradArgs &a, const OptConst &oc, const double (&acc)[CPL],
+                                           const VecF<CPL> &wv, const VecF<CPL> &av, size_t row_off) {
   VecF<CPL> wo;
   if constexpr (MODE == 0) {
-    const double lr = a.lr;
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) wo.v[c] = (float)__dsub_rn((double)wv.v[c], __dmul_rn(lr, acc[c]));
-    stg_frag<CPL>(wg, wo);
+    for (int c = 0; c < CPL; ++c) wo.v[c] = (float)__dsub_rn((double)wv.v[c], __dmul_rn(oc.lr, acc[c]));
+    stg_frag<CPL>(a.w + row_off, wo);
   } else {
     VecF<CPL> ao;
-    const float lrf = (float)a.lr, epsf = (float)a.eps;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       const double a64 = __dadd_rn((double)av.v[c], __dmul_rn(acc[c], acc[c]));
       const float af = (float)a64;
       const float g = (float)acc[c];
-      const float r = rcp_approx(sqrt_approx(af) + epsf);
+      const float r = rcp_approx(sqrt_approx(af) + oc.epsf);
       ao.v[c] = af;
-      wo.v[c] = wv.v[c] - (lrf * g) * r;
+      wo.v[c] = wv.v[c] - (oc.lrf * g) * r;
     }
-    stg_frag<CPL>(wg, wo);
-    stg_frag<CPL>(a.a + (size_t)lrow * a.dim + col, ao);
+    stg_frag<CPL>(a.w + row_off, wo);
+    stg_frag<CPL>(a.a + row_off, ao);
   }
 }
 
@@ -180,11 +185,11 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
     for (int c = 0; c < CPL; ++c) o.v[c] = (float)tot[c];
     stg_frag<CPL>(a.out_rows + (size_t)a.useg[pos] * D + col, o);
   } else {
-    const uint32_t lrow = key & a.lmask;
+    const size_t off = (size_t)(key & a.lmask) * D + col;
     VecF<CPL> wv, av;
-    ldg_frag<CPL>(wv, a.w + (size_t)lrow * D + col);
-    if (MODE == 1) ldg_frag<CPL>(av, a.a + (size_t)lrow * D + col);
-    apply_frag<CPL, MODE>(a, tot, wv, av, lrow, col);
+    ldg_frag<CPL>(wv, a.w + off);
+    if (MODE == 1) ldg_frag<CPL>(av, a.a + off);
+    apply_frag<CPL, MODE>(a, opt_const(a), tot, wv, av, off);
   }
 }
 
@@ -215,6 +220,7 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
   const int64_t p_hi = (p_lo + R < n) ? p_lo + R : n;
   if (p_lo >= p_hi) return;
   const float *src_base = a.src_mode == 0 ? a.dy : a.src;
+  const OptConst oc = opt_const(a);
 
   bool seen_head = false;  // a head was issued earlier in this range (=> open pieces began here)
   uint32_t kprev_carry = p_lo > 0 ? a.skey[p_lo - 1] : EMB_SENTINEL;
@@ -328,11 +334,10 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
 #pragma unroll
       for (int i = 0; i < T; ++i) {  // compile-time positions: constant shared offsets
         if (!((vmask >> i) & 1u)) continue;
-        if ((hmask >> i) & 1u) {
+        const bool hd = (hmask >> i) & 1u;
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) acc.v[c] = 0.0;
-          begins = true;
-        }
+        for (int c = 0; c < CPL; ++c) acc.v[c] = hd ? 0.0 : acc.v[c];
+        begins = begins || hd;
         VecF<CPL> v;
         if (active) lds_frag<CPL>(v, sbase + 4u * (uint32_t)(i * D));
         else v.zero();
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
                 VecF<CPL> wv, av;
                 lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((T + i) * D));
                 if (MODE == 1) lds_frag<CPL>(av, sbase + 4u * (uint32_t)((2 * T + i) * D));
-                apply_frag<CPL, MODE>(a, acc.v, wv, av, ki & a.lmask, col);
+                apply_frag<CPL, MODE>(a, oc, acc.v, wv, av, (size_t)(ki & a.lmask) * D + col);
               }
             }
           } else {
