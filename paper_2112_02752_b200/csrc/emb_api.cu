@@ -100,6 +100,9 @@ struct emb_ctx {
   float *gloc = nullptr;             // [max_ids][D]
   float *grecv = nullptr;            // [recv_cap][D]
   uint32_t *ok0 = nullptr, *ov0 = nullptr, *ok1 = nullptr, *ov1 = nullptr;  // owner sort buffers
+  uint32_t *sp = nullptr, *outidx = nullptr, *tcnt = nullptr;  // owner partition (segsort path)
+  bool ukey_is_g = false;        // requester unique keys are fused keys g (segsort path) or routing keys
+  bool owner_unique_done = false;
   uint32_t *ouseg = nullptr, *oukey = nullptr, *oustart = nullptr, *ouend = nullptr, *ou_count = nullptr,
            *ouniq_status = nullptr, *ouniq_counter = nullptr;  // owner-side dedup of the received keys
   int64_t *d_counts = nullptr;       // [2][EMB_MAX_WORLD] send, recv
@@ -361,6 +364,9 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
     bad |= dalloc(h, &h->ou_count, 2) != cudaSuccess;
     bad |= dalloc(h, &h->ouniq_status, unique_status_words(h->recv_cap)) != cudaSuccess;
     bad |= dalloc(h, &h->ouniq_counter, 1) != cudaSuccess;
+    bad |= dalloc(h, &h->sp, N) != cudaSuccess;
+    bad |= dalloc(h, &h->outidx, N) != cudaSuccess;
+    bad |= dalloc(h, &h->tcnt, (size_t)((N + 2047) / 2048 + 1) * EMB_MAX_WORLD) != cudaSuccess;
   }
   if (bad) return fail(h, EMB_ERR_NOMEM, "cannot allocate the step workspace");
   h->sws.hist = sort_words;
@@ -370,7 +376,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   h->sws.err = h->err_dev;
   CUDA_TRY(h, cudaMemset(h->tickets, 0, sizeof(uint32_t) * nticket));
   // table groups of the slot-major CSR (segsort fast path needs a non-decreasing slot_table)
-  if (W == 1) {
+  {
     h->segsort_ok = true;
     for (int s = 1; s < h->S; ++s)
       if (h->slot_table[s] < h->slot_table[s - 1]) h->segsort_ok = false;
@@ -575,15 +581,48 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   // ---------------- world > 1
   const int W = h->world;
   int nl = 0;
-  cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz, h->ks.key_bits, st,
-                                   &h->skey, &h->spay, &nl, prof_hook, h);
-  if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
-  h->launches += nl;
-  UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter};
-  LAUNCH(h, KID_UNIQUE, st, launch_unique(ua, st));
-  LAUNCH(h, KID_ROUTE, st, launch_owner_counts(h->ukey, h->u_count, W, h->ks.lbits, h->d_counts, st));
-  LAUNCH(h, KID_ROUTE, st, launch_scatter_inverse(h->skey, h->spay, h->useg, nnz, h->inv, st));
-  LAUNCH(h, KID_ROUTE, st, launch_local_of_unique(h->ukey, h->u_count, nnz, h->lmask, h->send_keys, st));
+  cudaError_t e = cudaSuccess;
+  if (h->segsort_ok) {
+    // per-table sort by fused key g, dedup, then a stable partition of the distinct keys by owner
+    SegSortArgs sa{};
+    sa.ids = ids;
+    sa.offsets = offsets;
+    sa.nnz = nnz;
+    sa.batch = batch;
+    sa.gslot = h->d_gslot;
+    sa.gbase = h->d_gbase;
+    sa.grows = h->d_grows;
+    sa.gbits = h->d_gbits;
+    sa.skey = h->k0;
+    sa.spay = h->v0;
+    sa.scratch_k = h->k1;
+    sa.scratch_a = h->v1;
+    sa.scratch_b = h->outidx;  // overwritten later in this step
+    sa.run_k = h->run_k;
+    sa.run_i = h->run_i;
+    sa.K = h->segK;
+    sa.err = h->err_dev;
+    h->skey = h->k0;
+    h->spay = h->v0;
+    if (batch > 0) LAUNCH(h, KID_SORT_PASS, st, launch_segsort(sa, h->G, st));
+    UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter};
+    LAUNCH(h, KID_UNIQUE, st, launch_unique(ua, st));
+    LAUNCH(h, KID_ROUTE, st,
+           launch_partition(h->ukey, h->u_count, nnz, h->ks, h->tcnt, h->send_keys, h->sp, h->d_counts, st));
+    LAUNCH(h, KID_ROUTE, st, launch_outidx(h->skey, h->spay, h->useg, h->sp, nnz, h->outidx, h->inv, st));
+    h->ukey_is_g = true;
+  } else {
+    e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz, h->ks.key_bits, st,
+                         &h->skey, &h->spay, &nl, prof_hook, h);
+    if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+    h->launches += nl;
+    UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter};
+    LAUNCH(h, KID_UNIQUE, st, launch_unique(ua, st));
+    LAUNCH(h, KID_ROUTE, st, launch_owner_counts(h->ukey, h->u_count, W, h->ks.lbits, h->d_counts, st));
+    LAUNCH(h, KID_ROUTE, st, launch_scatter_inverse(h->skey, h->spay, h->useg, nnz, h->inv, st));
+    LAUNCH(h, KID_ROUTE, st, launch_local_of_unique(h->ukey, h->u_count, nnz, h->lmask, h->send_keys, st));
+    h->ukey_is_g = false;
+  }
   // X0: per-peer counts
   {
     int64_t ones[EMB_MAX_WORLD], offs[EMB_MAX_WORLD];
@@ -612,20 +651,23 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   emb_status_t es = exchange(h, h->send_keys, h->send_counts, h->soff, h->recv_keys, h->recv_counts, h->roff,
                              sizeof(uint32_t), ncclUint32, 1, st);
   if (es != EMB_OK) return es;
-  // owner side: sort the received keys (stable: source-rank order inside a row) on the side stream
+  // owner side: the W received runs are each sorted by local id -> stable W-way merge (source-rank
+  // order inside a row) on the side stream, overlapped with the gather and X2
   CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
   CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-  e = radix_sort_pairs(h->sws, h->recv_keys, nullptr, h->ok0, h->ov0, h->ok1, h->ov1, h->n_recv, h->owner_key_bits,
-                       h->side, &h->okey, &h->opay, &nl, prof_hook, h);
-  if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("owner sort: ") + cudaGetErrorString(e));
-  h->launches += nl;
-  {
-    UniqueArgs ua{h->okey,        h->n_recv,   h->ouseg,         h->oukey,        h->oustart,
-                  h->ouend,       h->ou_count, h->ouniq_status, h->ouniq_counter};
-    LAUNCH(h, KID_UNIQUE, h->side, launch_unique(ua, h->side));
+  if (h->ukey_is_g || h->shard == 1) {
+    h->okey = h->ok0;
+    h->opay = h->ov0;
+    LAUNCH(h, KID_SORT_PASS, h->side,
+           launch_merge_runs(h->recv_keys, h->d_counts + EMB_MAX_WORLD, W, h->n_recv, h->okey, h->opay, h->err_dev,
+                             h->side));
+  } else {
+    e = radix_sort_pairs(h->sws, h->recv_keys, nullptr, h->ok0, h->ov0, h->ok1, h->ov1, h->n_recv, h->owner_key_bits,
+                         h->side, &h->okey, &h->opay, &nl, prof_hook, h);
+    if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("owner sort: ") + cudaGetErrorString(e));
+    h->launches += nl;
   }
-  // (the owner sort is the only user of the sort workspace while it runs: the requester sort finished
-  // before X1 on the main stream, and the next step's sort waits for the join below)
+  h->owner_unique_done = false;  // the owner-side dedup is only built on demand (step statistics)
   // gather requested rows and send them back
   LAUNCH(h, KID_OWNER_GATHER, st, launch_owner_gather(h->w, h->recv_keys, h->n_recv, h->D, h->owner_rows, st));
   es = exchange(h, h->owner_rows, h->recv_counts, h->roff, h->uniq_rows, h->send_counts, h->soff, sizeof(float),
@@ -689,6 +731,7 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
   g.src_mode = 0;
   g.sink_mode = 1;
   g.out_rows = h->gloc;
+  if (h->ukey_is_g) g.useg = h->outidx;  // merged gradient of a key goes to its send position
   LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
   emb_status_t es = exchange(h, h->gloc, h->send_counts, h->soff, h->grecv, h->recv_counts, h->roff, sizeof(float),
                              ncclFloat32, h->D, st);
@@ -723,6 +766,18 @@ emb_status_t ensure_unique(emb_ctx *h) {
   CUDA_TRY(h, cudaMemcpyAsync(&u, h->u_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaStreamSynchronize(st));
   h->U_l = u;
+  return EMB_OK;
+}
+
+// owner-side dedup of the merged received keys, built on demand (not part of the step)
+emb_status_t ensure_owner_unique(emb_ctx *h) {
+  if (h->world == 1 || h->owner_unique_done || h->n_recv <= 0) return EMB_OK;
+  cudaStream_t st = h->last_stream;
+  UniqueArgs ua{h->okey, h->n_recv, h->ouseg, h->oukey, h->oustart, h->ouend, h->ou_count, h->ouniq_status,
+                h->ouniq_counter};
+  CUDA_TRY(h, launch_unique(ua, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  h->owner_unique_done = true;
   return EMB_OK;
 }
 
@@ -959,6 +1014,8 @@ emb_status_t emb_last_step_info(emb_handle_t h, emb_step_info_t *info) {
       info->send_counts[p] = h->send_counts[p];
       info->recv_counts[p] = h->recv_counts[p];
     }
+    emb_status_t s2 = ensure_owner_unique(h);
+    if (s2 != EMB_OK) return s2;
     uint32_t u = 0;
     CUDA_TRY(h, cudaMemcpy(&u, h->ou_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
     info->unique_owner = h->n_recv > 0 ? u : 0;
@@ -974,7 +1031,7 @@ emb_status_t emb_last_unique(emb_handle_t h, uint64_t *keys_host, int64_t *count
   if (s != EMB_OK) return s;
   uint32_t U = 0;
   CUDA_TRY(h, cudaMemcpy(&U, h->u_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  return copy_unique(h, h->uend, h->ukey, h->ustart, U, true, false, keys_host, counts_host, cap, n_out);
+  return copy_unique(h, h->uend, h->ukey, h->ustart, U, !h->ukey_is_g, false, keys_host, counts_host, cap, n_out);
 }
 
 emb_status_t emb_last_owner_unique(emb_handle_t h, uint64_t *keys_host, int64_t *counts_host, int64_t cap,

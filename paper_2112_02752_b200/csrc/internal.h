@@ -194,6 +194,13 @@ struct SegSortArgs {
 cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st);
 cudaError_t launch_local_of_unique(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, uint32_t lmask,
                                    uint32_t *out, cudaStream_t st);
+cudaError_t launch_partition(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, const KeySpace &ks,
+                             uint32_t *tcnt, uint32_t *send_keys, uint32_t *sp, int64_t *send_counts,
+                             cudaStream_t st);
+cudaError_t launch_outidx(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, const uint32_t *sp,
+                          int64_t n, uint32_t *outidx, uint32_t *inv, cudaStream_t st);
+cudaError_t launch_merge_runs(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t n, uint32_t *okey,
+                              uint32_t *opay, uint32_t *err, cudaStream_t st);
 cudaError_t launch_owner_gather(const float *w, const uint32_t *local, int64_t n, int32_t dim, float *out,
                                 cudaStream_t st);
 
