@@ -43,6 +43,15 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def _traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed ncu capture, or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+        return d[kernel]["traffic_bytes"]
+    except Exception:
+        return None
+
+
 def workload_for(n_gpus: int):
     wl = synthgen.WORKLOADS["C2"] if n_gpus == 1 else synthgen.WORKLOADS["C3"]
     return wl
@@ -300,7 +309,7 @@ def main():
         t_launch = dom_ms / dom_cnt / 1e3
         ach = kb / t_launch / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": None, "launch_us": round(t_launch * 1e6, 2),
+                "frac": round(ach / peak, 4), "traffic": _traffic(dom) if n == 1 else None, "launch_us": round(t_launch * 1e6, 2),
                 "algorithmic_bytes_per_launch": int(kb), "peak_source": peak_src}
     kernels = {k: {"ms_total": round(v[0], 3), "launches": v[1], "us_per_launch": round(1e3 * v[0] / max(v[1], 1), 2)}
                for k, v in prof.items()}
