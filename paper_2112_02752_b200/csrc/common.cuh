@@ -9,6 +9,7 @@
 #define EMB_DEVERR_INVALID 0x2u
 #define EMB_DEVERR_RANGE 0x4u
 #define EMB_DEVERR_INTERNAL 0x8u  // a data-dependent address failed its bounds guard (bug)
+#define EMB_DEVERR_TIMEOUT 0x10u  // a peer never raised an exchange flag (world > 1)
 
 namespace emb {
 

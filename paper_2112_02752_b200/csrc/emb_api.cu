@@ -109,6 +109,15 @@ struct emb_ctx {
   int64_t *h_counts = nullptr;       // pinned [2*EMB_MAX_WORLD + 1]
   int64_t recv_cap = 0;
   ncclComm_t comm = nullptr;
+  // peer-memory exchange (p2p.cu): IPC-mapped peer buffers, epoch flags, device route table
+  bool use_p2p = false;
+  P2PArgs p2p{};
+  uint64_t epoch = 0;
+  int64_t *xmat = nullptr;
+  uint64_t *flags = nullptr;
+  RouteTable *rt = nullptr;
+  std::vector<void *> ipc_opened;
+  bool counts_synced = true;
 
   // ---- streams / step state
   cudaStream_t side = nullptr;
@@ -190,6 +199,8 @@ void prof_hook(void *vctx, int kid, int end, cudaStream_t st) {
 
 emb_status_t check_sticky(emb_ctx *h) {
   const uint32_t e = *(volatile uint32_t *)h->err_host;
+  if (e & EMB_DEVERR_TIMEOUT)
+    return fail(h, EMB_ERR_NCCL, "device: a peer never raised its exchange flag (sticky)");
   if (e & EMB_DEVERR_INTERNAL)
     return fail(h, EMB_ERR_CUDA, "device: an internal bounds guard tripped (library bug; work was skipped)");
   if (e & EMB_DEVERR_RANGE) return fail(h, EMB_ERR_RANGE, "device: an id was < 0 or >= rows[t] (sticky)");
@@ -210,6 +221,78 @@ int64_t local_of_global(const emb_ctx *h, uint64_t g) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// world > 1: map every peer's exchange buffers (CUDA IPC handles all-gathered over NCCL)
+emb_status_t setup_p2p(emb_ctx *h) {
+  const int W = h->world;
+  if (dalloc(h, &h->xmat, (size_t)P2P_MAXW * P2P_MAXW) || dalloc(h, &h->flags, (size_t)P2P_NKIND * P2P_MAXW) ||
+      dalloc(h, &h->rt, 1))
+    return fail(h, EMB_ERR_NOMEM, "alloc p2p state");
+  CUDA_TRY(h, cudaMemset(h->xmat, 0, sizeof(int64_t) * P2P_MAXW * P2P_MAXW));
+  CUDA_TRY(h, cudaMemset(h->flags, 0, sizeof(uint64_t) * P2P_NKIND * P2P_MAXW));
+  CUDA_TRY(h, cudaMemset(h->rt, 0, sizeof(RouteTable)));
+  constexpr int NB = 5;
+  void *mine[NB] = {h->xmat, h->flags, h->recv_keys, h->uniq_rows, h->grecv};
+  std::vector<cudaIpcMemHandle_t> hs(NB);
+  for (int b = 0; b < NB; ++b) CUDA_TRY(h, cudaIpcGetMemHandle(&hs[b], mine[b]));
+  const size_t bytes = sizeof(cudaIpcMemHandle_t) * NB;
+  char *dsend = nullptr, *drecv = nullptr;
+  CUDA_TRY(h, cudaMalloc(&dsend, bytes));
+  CUDA_TRY(h, cudaMalloc(&drecv, bytes * W));
+  CUDA_TRY(h, cudaMemcpy(dsend, hs.data(), bytes, cudaMemcpyHostToDevice));
+  NCCL_TRY(h, ncclAllGather(dsend, drecv, bytes, ncclUint8, h->comm, 0));
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  std::vector<cudaIpcMemHandle_t> all((size_t)NB * W);
+  CUDA_TRY(h, cudaMemcpy(all.data(), drecv, bytes * W, cudaMemcpyDeviceToHost));
+  cudaFree(dsend);
+  cudaFree(drecv);
+  P2PArgs &p = h->p2p;
+  p.world = W;
+  p.rank = h->rank;
+  p.flags = h->flags;
+  p.xmat = h->xmat;
+  p.rt = h->rt;
+  for (int r = 0; r < W; ++r) {
+    void *ptr[NB];
+    for (int b = 0; b < NB; ++b) {
+      if (r == h->rank) {
+        ptr[b] = mine[b];
+      } else {
+        void *q = nullptr;
+        CUDA_TRY(h, cudaIpcOpenMemHandle(&q, all[(size_t)r * NB + b], cudaIpcMemLazyEnablePeerAccess));
+        h->ipc_opened.push_back(q);
+        ptr[b] = q;
+      }
+    }
+    p.peer_xmat[r] = static_cast<int64_t *>(ptr[0]);
+    p.peer_flags[r] = static_cast<uint64_t *>(ptr[1]);
+    p.peer_recv_keys[r] = static_cast<uint32_t *>(ptr[2]);
+    p.peer_uniq_rows[r] = static_cast<float *>(ptr[3]);
+    p.peer_grecv[r] = static_cast<float *>(ptr[4]);
+  }
+  return EMB_OK;
+}
+
+// p2p mode: bring the step's counts (device route table) to the host, for statistics only
+emb_status_t sync_counts(emb_ctx *h) {
+  if (h->counts_synced) return EMB_OK;
+  if (h->last_stream) CUDA_TRY(h, cudaStreamSynchronize(h->last_stream));
+  RouteTable rt;
+  CUDA_TRY(h, cudaMemcpy(&rt, h->rt, sizeof(rt), cudaMemcpyDeviceToHost));
+  const int W = h->world;
+  for (int p = 0; p <= W; ++p) {
+    h->soff[p] = rt.soff[p];
+    h->roff[p] = rt.roff[p];
+  }
+  for (int p = 0; p < W; ++p) {
+    h->send_counts[p] = rt.soff[p + 1] - rt.soff[p];
+    h->recv_counts[p] = rt.recv_counts[p];
+  }
+  h->U_l = rt.n_send;
+  h->n_recv = rt.n_recv;
+  h->counts_synced = true;
+  return EMB_OK;
+}
+
 emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   if (!cfg) return fail(h, EMB_ERR_INVALID, "cfg is NULL");
   if (cfg->num_tables < 1 || cfg->num_tables > EMB_MAX_TABLES || !cfg->rows)
@@ -426,6 +509,12 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
     ncclUniqueId id;
     std::memcpy(&id, cfg->nccl_id, sizeof(id));
     NCCL_TRY(h, ncclCommInitRank(&h->comm, W, id, h->rank));
+    const char *ex = getenv("EMB_EXCHANGE");  // "nccl" selects the v1 grouped send/recv exchange
+    h->use_p2p = h->segsort_ok && !(ex && std::strcmp(ex, "nccl") == 0);
+    if (h->use_p2p) {
+      emb_status_t ps = setup_p2p(h);
+      if (ps != EMB_OK) return ps;
+    }
   }
   CUDA_TRY(h, cudaStreamSynchronize(h->side));
   CUDA_TRY(h, cudaDeviceSynchronize());
@@ -436,6 +525,7 @@ void destroy_impl(emb_ctx *h) {
   if (!h) return;
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
+  for (void *p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   if (h->comm) ncclCommDestroy(h->comm);
   for (void *p : h->allocs) cudaFree(p);
   if (h->err_host) cudaFreeHost(h->err_host);
@@ -623,6 +713,41 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     LAUNCH(h, KID_ROUTE, st, launch_local_of_unique(h->ukey, h->u_count, nnz, h->lmask, h->send_keys, st));
     h->ukey_is_g = false;
   }
+  if (h->use_p2p) {
+    // ---- peer-memory exchange: no host synchronisation
+    P2PArgs px = h->p2p;
+    px.epoch = ++h->epoch;
+    const int64_t cap = h->recv_cap;
+    LAUNCH(h, KID_NCCL, st, launch_xcounts(px, h->d_counts, st));
+    LAUNCH(h, KID_NCCL, st, launch_wait(px, P2P_COUNTS, h->err_dev, st));
+    LAUNCH(h, KID_ROUTE, st, launch_push_keys(px, h->send_keys, nnz, st));
+    LAUNCH(h, KID_NCCL, st, launch_signal(px, P2P_KEYS, st));
+    LAUNCH(h, KID_NCCL, st, launch_wait(px, P2P_KEYS, h->err_dev, st));
+    // owner side: stable W-way merge of the received runs, overlapped with the gather-push
+    CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    h->okey = h->ok0;
+    h->opay = h->ov0;
+    LAUNCH(h, KID_SORT_PASS, h->side,
+           launch_merge_runs(h->recv_keys, h->rt->recv_counts, W, cap, h->okey, h->opay, h->err_dev, h->side));
+    LAUNCH(h, KID_OWNER_GATHER, st,
+           launch_gather_push(px, h->w, h->recv_keys, h->D, cap, h->rows_local, h->err_dev, st));
+    LAUNCH(h, KID_NCCL, st, launch_signal(px, P2P_ROWS, st));
+    LAUNCH(h, KID_NCCL, st, launch_wait(px, P2P_ROWS, h->err_dev, st));
+    pa.rows_src = h->uniq_rows;
+    pa.nrows_src = h->max_ids;
+    pa.row_idx = h->inv;
+    if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
+    CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
+    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
+    if (batch > 0) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
+    h->counts_synced = false;
+    h->U_l = -1;
+    h->n_recv = -1;
+    h->owner_unique_done = false;
+    h->state = 1;
+    return EMB_OK;
+  }
   // X0: per-peer counts
   {
     int64_t ones[EMB_MAX_WORLD], offs[EMB_MAX_WORLD];
@@ -724,6 +849,37 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
     h->state = 0;
     return EMB_OK;
   }
+  if (h->use_p2p) {
+    // requester: merged per-key gradients stored straight into the owners' receive buffers (fused X3)
+    P2PArgs px = h->p2p;
+    px.epoch = h->epoch;
+    g.skey = h->skey;
+    g.spay = h->spay;
+    g.n = h->nnz;
+    g.src_mode = 0;
+    g.sink_mode = 2;
+    g.useg = h->outidx;
+    g.nout = h->max_ids;
+    g.p2p = px;
+    LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
+    LAUNCH(h, KID_NCCL, st, launch_signal(px, P2P_GRADS, st));
+    LAUNCH(h, KID_NCCL, st, launch_wait(px, P2P_GRADS, h->err_dev, st));
+    // owner: merge the W sources' gradients per row (source-rank order) and apply
+    GradArgs o = g;
+    o.skey = h->okey;
+    o.spay = h->opay;
+    o.n = h->recv_cap;
+    o.n_dev = &h->rt->n_recv;
+    o.src_mode = 1;
+    o.src = h->grecv;
+    o.nsrc = h->recv_cap;
+    o.blen = nullptr;
+    o.sink_mode = 0;
+    o.lmask = 0xFFFFFFFFu;
+    LAUNCH(h, KID_GRAD_APPLY, st, launch_grad(o, st));
+    h->state = 0;
+    return EMB_OK;
+  }
   // requester: per-unique-key local gradient (fp32 rows in unique order = owner-grouped send order)
   g.skey = h->skey;
   g.spay = h->spay;
@@ -757,7 +913,8 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
 
 // host-side unique of the last step (runs the GPU dedup kernel if the step did not)
 emb_status_t ensure_unique(emb_ctx *h) {
-  if (h->world > 1 || h->U_l >= 0) return EMB_OK;
+  if (h->world > 1) return sync_counts(h);
+  if (h->U_l >= 0) return EMB_OK;
   // world == 1: the step itself never needs the compacted unique list; build it on demand
   cudaStream_t st = h->last_stream;
   UniqueArgs ua{h->skey, h->nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter};
@@ -771,6 +928,10 @@ emb_status_t ensure_unique(emb_ctx *h) {
 
 // owner-side dedup of the merged received keys, built on demand (not part of the step)
 emb_status_t ensure_owner_unique(emb_ctx *h) {
+  if (h->world > 1) {
+    emb_status_t s = sync_counts(h);
+    if (s != EMB_OK) return s;
+  }
   if (h->world == 1 || h->owner_unique_done || h->n_recv <= 0) return EMB_OK;
   cudaStream_t st = h->last_stream;
   UniqueArgs ua{h->okey, h->n_recv, h->ouseg, h->oukey, h->oustart, h->ouend, h->ou_count, h->ouniq_status,

@@ -105,6 +105,20 @@ __device__ __forceinline__ void apply_frag(const GradArgs &a, const OptConst &oc
   }
 }
 
+// destination row of a merged per-key gradient (MODE 2: local X3 send buffer; MODE 3: the owner's
+// receive buffer through peer memory, at my offset there + the key's position in my send order)
+template <int MODE>
+__device__ __forceinline__ float *out_row(const GradArgs &a, uint32_t ui, int D) {
+  if constexpr (MODE == 3) {
+    const RouteTable *rt = a.p2p.rt;
+    int d = 0;
+    while (d + 1 < a.p2p.world && (int64_t)ui >= rt->soff[d + 1]) ++d;
+    return a.p2p.peer_grecv[d] + (size_t)(rt->dst_off[d] + ((int64_t)ui - rt->soff[d])) * D;
+  } else {
+    return a.out_rows + (size_t)ui * D;
+  }
+}
+
 // warp-parallel gallop: first (dir = -1) or last (dir = +1) position of the segment of key k that
 // contains position p (all lanes call; one L2 round trip per 32x of distance)
 __device__ int64_t seg_bound_warp(const uint32_t *skey, int64_t n, int64_t p, uint32_t k, int dir) {
@@ -140,7 +154,7 @@ __device__ int64_t seg_bound_warp(const uint32_t *skey, int64_t n, int64_t p, ui
 // warp sums the partials in warp order and sinks the total. (Rare path: <= 2 per warp; not inlined.)
 template <int CPL, int MODE>
 __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, int64_t slot, int64_t pos,
-                                        uint32_t key, int64_t R) {
+                                        uint32_t key, int64_t R, int64_t n) {
   const int lane = threadIdx.x & 31;
   const int D = a.dim;
   const int col = lane * CPL;
@@ -151,8 +165,8 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
     for (int c = 0; c < CPL; c += 2)
       __stcg(reinterpret_cast<double2 *>(dst + c), make_double2(acc.v[c], acc.v[c + 1]));
   }
-  const int64_t first = seg_bound_warp(a.skey, a.n, pos, key, -1);
-  const int64_t lastp = seg_bound_warp(a.skey, a.n, pos, key, +1);
+  const int64_t first = seg_bound_warp(a.skey, n, pos, key, -1);
+  const int64_t lastp = seg_bound_warp(a.skey, n, pos, key, +1);
   __threadfence();
   __syncwarp();
   int last = 0;
@@ -179,11 +193,12 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
       tot[c + 1] = __dadd_rn(tot[c + 1], v.y);
     }
   }
-  if constexpr (MODE == 2) {
+  if constexpr (MODE >= 2) {
     VecF<CPL> o;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) o.v[c] = (float)tot[c];
-    stg_frag<CPL>(a.out_rows + (size_t)a.useg[pos] * D + col, o);
+    stg_frag<CPL>(out_row<MODE>(a, a.useg[pos], D) + col, o);
+    if (MODE == 3) __threadfence_system();
   } else {
     const size_t off = (size_t)(key & a.lmask) * D + col;
     VecF<CPL> wv, av;
@@ -205,6 +220,7 @@ template <int CPL, int T, int NS, bool MEAN, int MODE, int DC>
 __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NA = (MODE == 1) ? 3 : (MODE == 0 ? 2 : 1);  // row arrays per stage: contribution, w, a
+  constexpr bool SINK_OPT = MODE < 2;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int D = DC ? DC : a.dim;  // compile-time row width for D = 64 / 128 / 256
   const int col = lane * CPL;
@@ -214,7 +230,7 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
   const uint32_t wbase = smem_u32(smem) + (uint32_t)(wib * NS * stage_floats * 4);
   const int64_t gw = ((int64_t)blockIdx.x * (blockDim.x >> 5)) + wib;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t n = a.n;
+  const int64_t n = a.n_dev ? *a.n_dev : a.n;
   const int64_t R = (n + nwarps - 1) / nwarps;
   const int64_t p_lo = gw * R;
   const int64_t p_hi = (p_lo + R < n) ? p_lo + R : n;
@@ -251,8 +267,8 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
     if (k != EMB_SENTINEL) {
       if ((int64_t)srow >= a.nsrc) bad = true;
       else if (MEAN) len = a.blen[srow];
-      if (MODE != 2 && (int64_t)(k & a.lmask) >= a.nrows) bad = true;
-      if (MODE == 2) {
+      if (SINK_OPT && (int64_t)(k & a.lmask) >= a.nrows) bad = true;
+      if (!SINK_OPT) {
         uo = a.useg[t0 + lane];
         if ((int64_t)uo >= a.nout) bad = true;
       }
@@ -268,7 +284,7 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
     m.hmask = __ballot_sync(0xffffffffu, head);
     m.tmask = __ballot_sync(0xffffffffu, tail);
     const uint32_t le_mask = (lane < 31) ? ((2u << lane) - 1u) : 0xFFFFFFFFu;
-    const bool applies = MODE != 2 && tail && (((m.hmask & le_mask) != 0) || seen_head);
+    const bool applies = SINK_OPT && tail && (((m.hmask & le_mask) != 0) || seen_head);
     const uint32_t amask = __ballot_sync(0xffffffffu, applies);
     seen_head = seen_head || m.hmask != 0;
     kprev_carry = __shfl_sync(0xffffffffu, k, cnt - 1);
@@ -286,7 +302,7 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
       const unsigned long long wri = __shfl_sync(0xffffffffu, wrow, il);
       const uint32_t off = (uint32_t)((i * D + c * 4) * 4);
       if (i < T && ((m.vmask >> i) & 1u)) cp_async16(sb + off, src_base + (size_t)ri * D + c * 4);
-      if (MODE != 2 && i < T && ((amask >> i) & 1u)) {
+      if (SINK_OPT && i < T && ((amask >> i) & 1u)) {
         cp_async16(sb + (uint32_t)(T * D * 4) + off, a.w + wri + c * 4);
         if (MODE == 1) cp_async16(sb + (uint32_t)(2 * T * D * 4) + off, a.a + wri + c * 4);
       }
@@ -354,13 +370,13 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
         if ((tmask >> i) & 1u) {
           const uint32_t ki = __shfl_sync(0xffffffffu, m.key, i);
           if (begins) {  // complete inside the range
-            if constexpr (MODE == 2) {
+            if constexpr (!SINK_OPT) {
               const uint32_t ui = __shfl_sync(0xffffffffu, m.uo, i);
               if (active) {
                 VecF<CPL> o;
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) o.v[c] = (float)acc.v[c];
-                stg_frag<CPL>(a.out_rows + (size_t)ui * D + col, o);
+                stg_frag<CPL>(out_row<MODE>(a, ui, D) + col, o);
               }
             } else {
               if (active) {
@@ -371,7 +387,7 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
               }
             }
           } else {
-            span_piece<CPL, MODE>(a, acc, 2 * gw, t0 + i, ki, R);  // continuation piece that ends here
+            span_piece<CPL, MODE>(a, acc, 2 * gw, t0 + i, ki, R, n);  // continuation piece that ends here
           }
 #pragma unroll
           for (int c = 0; c < CPL; ++c) acc.v[c] = 0.0;
@@ -402,7 +418,8 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
     }
   }
   cp_async_wait<0>();
-  if (open) span_piece<CPL, MODE>(a, acc, begins ? 2 * gw + 1 : 2 * gw, open_pos, open_key, R);  // continues past the range
+  if (open) span_piece<CPL, MODE>(a, acc, begins ? 2 * gw + 1 : 2 * gw, open_pos, open_key, R, n);  // continues past the range
+  if (MODE == 3) __threadfence_system();  // peer stores of this thread precede the GRADS flag
 }
 
 static int g_sms = 0;
@@ -436,15 +453,17 @@ static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
 template <int CPL, int T, int DC>
 static cudaError_t launch_grad_d(const GradArgs &a, cudaStream_t st) {
   const bool mean = a.blen != nullptr;
-  const int mode = a.sink_mode == 1 ? 2 : (a.opt == 1 ? 1 : 0);
+  const int mode = a.sink_mode == 2 ? 3 : (a.sink_mode == 1 ? 2 : (a.opt == 1 ? 1 : 0));
   if (mean) {
     if (mode == 0) return launch_grad_t<CPL, T, 2, true, 0, DC>(a, st);
     if (mode == 1) return launch_grad_t<CPL, T, 2, true, 1, DC>(a, st);
-    return launch_grad_t<CPL, T, 2, true, 2, DC>(a, st);
+    if (mode == 2) return launch_grad_t<CPL, T, 2, true, 2, DC>(a, st);
+    return launch_grad_t<CPL, T, 2, true, 3, DC>(a, st);
   }
   if (mode == 0) return launch_grad_t<CPL, T, 2, false, 0, DC>(a, st);
   if (mode == 1) return launch_grad_t<CPL, T, 2, false, 1, DC>(a, st);
-  return launch_grad_t<CPL, T, 2, false, 2, DC>(a, st);
+  if (mode == 2) return launch_grad_t<CPL, T, 2, false, 2, DC>(a, st);
+  return launch_grad_t<CPL, T, 2, false, 3, DC>(a, st);
 }
 
 int64_t grad_max_warps(int dev) {

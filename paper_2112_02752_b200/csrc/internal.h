@@ -52,6 +52,36 @@ enum KernelId {
   KID_COUNT
 };
 
+// ---- world > 1 peer-memory exchange (p2p.cu) ------------------------------------------------------
+constexpr int P2P_MAXW = 16;  // == EMB_MAX_WORLD
+enum { P2P_COUNTS = 0, P2P_KEYS = 1, P2P_ROWS = 2, P2P_GRADS = 3, P2P_NKIND = 4 };
+struct RouteTable {               // device-resident, rebuilt every step from the count matrix
+  int64_t soff[P2P_MAXW + 1];     // my send buffer: start of owner d's keys
+  int64_t roff[P2P_MAXW + 1];     // my receive buffer: start of source s's run
+  int64_t dst_off[P2P_MAXW];      // where my keys / gradients start in owner d's receive buffer
+  int64_t src_off[P2P_MAXW];      // where my rows start in requester s's row buffer
+  int64_t recv_counts[P2P_MAXW];
+  int64_t n_recv, n_send;
+};
+struct P2PArgs {
+  int32_t world, rank;
+  uint64_t epoch;
+  uint64_t *flags;                 // own [P2P_NKIND][P2P_MAXW]
+  int64_t *xmat;                   // own [W][W]
+  RouteTable *rt;
+  int64_t *peer_xmat[P2P_MAXW];
+  uint64_t *peer_flags[P2P_MAXW];
+  uint32_t *peer_recv_keys[P2P_MAXW];
+  float *peer_uniq_rows[P2P_MAXW];
+  float *peer_grecv[P2P_MAXW];
+};
+cudaError_t launch_xcounts(const P2PArgs &a, const int64_t *send_counts, cudaStream_t st);
+cudaError_t launch_signal(const P2PArgs &a, int kind, cudaStream_t st);
+cudaError_t launch_wait(const P2PArgs &a, int kind, uint32_t *err, cudaStream_t st);
+cudaError_t launch_push_keys(const P2PArgs &a, const uint32_t *send_keys, int64_t cap, cudaStream_t st);
+cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t *recv_keys, int dim, int64_t cap,
+                               int64_t rows_local, uint32_t *err, cudaStream_t st);
+
 // ---- launchers (each returns cudaGetLastError()) ------------------------------------------------
 struct KeysArgs {
   const int64_t *ids;
@@ -127,8 +157,11 @@ struct GradArgs {
   int32_t batch, num_slots;
   const float *src;        // mode 1
   // sink: mode 0 = optimizer apply on table rows (local row = key & lmask); mode 1 = write fp32 row
-  // to out_rows[useg[p]] (requester-side local grad)
+  // to out_rows[useg[p]] (requester-side local grad); mode 2 = the same row stored straight into the
+  // owner's gradient buffer through peer memory (p2p exchange)
   int32_t sink_mode;
+  const int64_t *n_dev;    // if set, the number of sorted positions is read from the device
+  P2PArgs p2p;             // sink mode 2
   uint32_t lmask;
   int32_t opt;             // 0 sgd 1 adagrad
   double lr, eps;
