@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -478,10 +479,12 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
       }
       gslot.push_back(h->S);
       h->G = (int32_t)gbase.size();
-      // key ranges (CTAs) per group: ~2K occurrences per CTA at the capacity bound; every CTA scans
+      // key ranges (CTAs) per group: ~4K occurrences per CTA at the capacity bound (K sweep on C2:
+      // K=2/4/8/16 -> 206/157/176/201 us per step); every CTA scans
       // its whole group, so K stays small
       const int64_t per = (h->max_ids + h->G - 1) / h->G;
-      h->segK = (int32_t)std::min<int64_t>(16, std::max<int64_t>(1, (per + 2047) / 2048));
+      h->segK = (int32_t)std::min<int64_t>(16, std::max<int64_t>(1, (per + 4095) / 4096));
+      if (const char *ek = getenv("EMB_SEGK")) h->segK = std::max(1, std::min(32, atoi(ek)));  // experiment knob
       if (dalloc(h, &h->run_k, h->max_ids) || dalloc(h, &h->run_i, h->max_ids))
         return fail(h, EMB_ERR_NOMEM, "alloc sort runs");
       if (dalloc(h, &h->d_gslot, gslot.size()) || dalloc(h, &h->d_gbase, h->G) || dalloc(h, &h->d_grows, h->G) ||
