@@ -216,8 +216,8 @@ struct TileMeta {
   uint32_t vmask, hmask, tmask;  // warp-uniform: valid / head / tail
 };
 
-template <int CPL, int T, int NS, bool MEAN, int MODE, int DC>
-__global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a) {
+template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ GradArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NA = (MODE == 1) ? 3 : (MODE == 0 ? 2 : 1);  // row arrays per stage: contribution, w, a
   constexpr bool SINK_OPT = MODE < 2;
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(256) k_grad(const __grid_constant__ GradArgs a
 
 static int g_sms = 0;
 
-template <int CPL, int T, int NS, bool MEAN, int MODE, int DC>
+template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2>
 static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
   constexpr int NA = (MODE == 1) ? 3 : (MODE == 0 ? 2 : 1);
   const size_t per_warp = (size_t)NS * NA * T * a.dim * sizeof(float);
@@ -435,18 +435,18 @@ static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
   static size_t attr = 0;
   if (attr < smem) {
     cudaError_t e =
-        cudaFuncSetAttribute(k_grad<CPL, T, NS, MEAN, MODE, DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_grad<CPL, T, NS, MEAN, MODE, DC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grad<CPL, T, NS, MEAN, MODE, DC>, wpc * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grad<CPL, T, NS, MEAN, MODE, DC, MINB>, wpc * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)g_sms * per_sm;
   const int64_t max_blocks = ((a.n + 4 * T - 1) / (4 * T) + wpc - 1) / wpc;  // >= 4 tiles per warp
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  k_grad<CPL, T, NS, MEAN, MODE, DC><<<(unsigned)blocks, wpc * 32, smem, st>>>(a);
+  k_grad<CPL, T, NS, MEAN, MODE, DC, MINB><<<(unsigned)blocks, wpc * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -478,6 +478,17 @@ cudaError_t launch_grad(const GradArgs &a, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (a.dim == 64 && a.blen == nullptr && a.sink_mode == 0 && a.opt == 1) {
+    static int var = -1;  // experiment knob for the C2 path: tile size x register cap
+    if (var < 0) {
+      const char *v = getenv("EMB_GRAD_VAR");
+      var = v ? atoi(v) : 0;
+    }
+    if (var == 1) return launch_grad_t<2, 4, 2, false, 1, 64, 3>(a, st);
+    if (var == 2) return launch_grad_t<2, 8, 2, false, 1, 64, 3>(a, st);
+    if (var == 3) return launch_grad_t<2, 16, 2, false, 1, 64, 1>(a, st);
+    if (var == 4) return launch_grad_t<2, 4, 2, false, 1, 64, 4>(a, st);
   }
   if (a.dim == 64) return launch_grad_d<2, 8, 64>(a, st);
   if (a.dim == 128) return launch_grad_d<4, 8, 128>(a, st);
