@@ -13,6 +13,8 @@
 //  * other tiles: the warp walks the flattened occurrence range of its 32 bags in batches of RCH
 //    rows (keys of the next batch prefetched), accumulating in fp64 and flushing each bag at its end.
 // One tile per warp (grid-stride loop kept for very large batches).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "internal.h"
 #include "vec.cuh"
@@ -119,9 +121,9 @@ __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, in
   while (cb < nbt) flush();
 }
 
-template <int CPL>
-__global__ void __launch_bounds__(POOL_THREADS, 3) k_pool(const __grid_constant__ PoolArgs a) {
-  constexpr int RCH = 32 / CPL;  // rows per batch: 32 floats in flight per lane
+template <int CPL, int RCH, int MINB>
+__global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_constant__ PoolArgs a) {
+  // RCH rows per batch of the single-id path (RCH * CPL floats in flight per lane)
   const int lane = threadIdx.x & 31;
   const int D = a.dim;
   const int col = lane * CPL;
@@ -180,12 +182,12 @@ __global__ void __launch_bounds__(POOL_THREADS, 3) k_pool(const __grid_constant_
   }
 }
 
-template <int CPL>
+template <int CPL, int RCH, int MINB>
 static cudaError_t launch_pool_t(const PoolArgs &a, int64_t ntiles, cudaStream_t st) {
   // one tile per warp (not persistent), so the concurrent side-stream sort CTAs get SMs as soon as
   // they are ready and the pool fills the rest
   const int64_t blocks = (ntiles * 32 + POOL_THREADS - 1) / POOL_THREADS;
-  k_pool<CPL><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
+  k_pool<CPL, RCH, MINB><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -202,9 +204,19 @@ cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st) {
   const int64_t nb = (int64_t)a.num_slots * a.batch;
   if (nb == 0) return cudaSuccess;
   const int64_t ntiles = (nb + 31) / 32;
-  if (a.dim <= 64) return launch_pool_t<2>(a, ntiles, st);
-  if (a.dim <= 128) return launch_pool_t<4>(a, ntiles, st);
-  return launch_pool_t<8>(a, ntiles, st);
+  static int var = -1;
+  if (var < 0) {
+    const char *v = getenv("EMB_POOL_VAR");  // experiment knob (D <= 64): rows in flight x register cap
+    var = v ? atoi(v) : 0;
+  }
+  if (a.dim <= 64) {
+    if (var == 1) return launch_pool_t<2, 32, 2>(a, ntiles, st);
+    if (var == 2) return launch_pool_t<2, 32, 3>(a, ntiles, st);
+    if (var == 3) return launch_pool_t<2, 8, 4>(a, ntiles, st);
+    return launch_pool_t<2, 16, 3>(a, ntiles, st);
+  }
+  if (a.dim <= 128) return launch_pool_t<4, 8, 3>(a, ntiles, st);
+  return launch_pool_t<8, 4, 3>(a, ntiles, st);
 }
 
 }  // namespace emb

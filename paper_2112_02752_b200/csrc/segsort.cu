@@ -67,13 +67,23 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_const
   const uint32_t base = (uint32_t)a.gbase[g];
   const uint32_t rows = a.grows[g];
   const uint32_t bits = a.gbits[g];
-  const uint64_t mul = ((uint64_t)K << 32) / ((uint64_t)rows + 1u);
+  // bucket(lk) = floor(lk * mul / 2^32), mul = floor(2^32 K / (rows + 1)) < 2^32: one IMAD.HI, monotone
+  const uint32_t mul = (uint32_t)((((uint64_t)K) << 32) / ((uint64_t)rows + 1u));
   // table-local id; invalid ids (R4) become `rows` and sort to the end of the group
   auto local_of = [&](int64_t id) { return (id >= 0 && id < (int64_t)rows) ? (uint32_t)id : rows; };
   auto bucket_of = [&](uint32_t lk) {
-    const uint32_t b = (uint32_t)(((uint64_t)lk * mul) >> 32);
+    const uint32_t b = __umulhi(lk, mul);
     return b < (uint32_t)K ? b : (uint32_t)K - 1u;
   };
+  // stage the whole group's local ids in shared memory once (both scans below read them twice)
+  const bool staged = ng <= (uint32_t)SEG_CAP;
+  uint32_t *gk = sm + 4 * SEG_CHUNK_CAP;  // [SEG_CAP] after the range buffers
+  if (staged) {
+#pragma unroll 4
+    for (uint32_t i = tid; i < ng; i += SS_THREADS) gk[i] = local_of(a.ids[glo + i]);
+    __syncthreads();
+  }
+  auto key_at = [&](uint32_t i) -> uint32_t { return staged ? gk[i] : local_of(a.ids[glo + i]); };
   // ---- 1. count: items below / inside this range, per warp over a contiguous 1/16 of the group
   const uint32_t span = ((ng + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;
   const uint32_t s_lo = w * span, s_hi = min(ng, s_lo + span);
@@ -81,7 +91,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_const
   for (uint32_t r0 = s_lo; r0 < s_hi; r0 += 32) {
     const uint32_t i = r0 + lane;
     uint32_t bb = 0xFFFFFFFFu;
-    if (i < s_hi) bb = bucket_of(local_of(a.ids[glo + i]));
+    if (i < s_hi) bb = bucket_of(key_at(i));
     below += __popc(__ballot_sync(0xffffffffu, bb < (uint32_t)bkt));
     mine += __popc(__ballot_sync(0xffffffffu, bb == (uint32_t)bkt));
   }
@@ -115,7 +125,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_const
       uint32_t lk = 0;
       bool in = false;
       if (i < s_hi) {
-        lk = local_of(a.ids[glo + i]);
+        lk = key_at(i);
         in = bucket_of(lk) == (uint32_t)bkt;
       }
       const uint32_t m = __ballot_sync(0xffffffffu, in);
@@ -322,7 +332,7 @@ __global__ void __launch_bounds__(1024, 1) k_segsort_cta(const __grid_constant__
   }
 }
 
-size_t segsort_smem_bytes() { return (size_t)SEG_CHUNK_CAP * 16; }
+size_t segsort_smem_bytes() { return (size_t)SEG_CHUNK_CAP * 16 + (size_t)SEG_CAP * 4; }
 
 cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st) {
   if (groups <= 0 || a.nnz <= 0) return cudaSuccess;
