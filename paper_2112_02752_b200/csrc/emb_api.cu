@@ -38,7 +38,8 @@ std::string g_create_error = "no error";
 
 const char *kKernelNames[KID_COUNT] = {"keys",        "sort_hist",  "sort_pass", "pool",
                                        "grad_apply",  "unique",     "route",     "owner_gather",
-                                       "grad_local",  "nccl",       "init"};
+                                       "grad_local",  "nccl",       "init",      "owner_merge",
+                                       "p2p_wait"};
 
 uint32_t bits_for(uint64_t x) {  // smallest b with x < 2^b (x >= 0)
   uint32_t b = 0;
@@ -117,6 +118,7 @@ struct emb_ctx {
   int64_t *xmat = nullptr;
   uint64_t *flags = nullptr;
   RouteTable *rt = nullptr;
+  uint32_t *p2p_done = nullptr;
   std::vector<void *> ipc_opened;
   bool counts_synced = true;
 
@@ -226,8 +228,9 @@ int64_t local_of_global(const emb_ctx *h, uint64_t g) {
 emb_status_t setup_p2p(emb_ctx *h) {
   const int W = h->world;
   if (dalloc(h, &h->xmat, (size_t)P2P_MAXW * P2P_MAXW) || dalloc(h, &h->flags, (size_t)P2P_NKIND * P2P_MAXW) ||
-      dalloc(h, &h->rt, 1))
+      dalloc(h, &h->rt, 1) || dalloc(h, &h->p2p_done, (size_t)P2P_NKIND))
     return fail(h, EMB_ERR_NOMEM, "alloc p2p state");
+  CUDA_TRY(h, cudaMemset(h->p2p_done, 0, sizeof(uint32_t) * P2P_NKIND));
   CUDA_TRY(h, cudaMemset(h->xmat, 0, sizeof(int64_t) * P2P_MAXW * P2P_MAXW));
   CUDA_TRY(h, cudaMemset(h->flags, 0, sizeof(uint64_t) * P2P_NKIND * P2P_MAXW));
   CUDA_TRY(h, cudaMemset(h->rt, 0, sizeof(RouteTable)));
@@ -252,6 +255,7 @@ emb_status_t setup_p2p(emb_ctx *h) {
   p.flags = h->flags;
   p.xmat = h->xmat;
   p.rt = h->rt;
+  p.done = h->p2p_done;
   for (int r = 0; r < W; ++r) {
     void *ptr[NB];
     for (int b = 0; b < NB; ++b) {
@@ -607,6 +611,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   if (batch > 0 && !direct) LAUNCH(h, KID_KEYS, st, launch_keys(ka, st));
 
   PoolArgs pa{};
+  pa.wait_kind = -1;
   pa.key = h->key_csr;
   pa.offsets = offsets;
   pa.nnz = nnz;
@@ -721,22 +726,21 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     P2PArgs px = h->p2p;
     px.epoch = ++h->epoch;
     const int64_t cap = h->recv_cap;
-    LAUNCH(h, KID_NCCL, st, launch_xcounts(px, h->d_counts, st));
-    LAUNCH(h, KID_NCCL, st, launch_wait(px, P2P_COUNTS, h->err_dev, st));
+    // X0 (counts + wait + route table), X1 (keys; its last block raises KEYS)
+    LAUNCH(h, KID_NCCL, st, launch_xcounts(px, h->d_counts, h->err_dev, st));
     LAUNCH(h, KID_ROUTE, st, launch_push_keys(px, h->send_keys, nnz, st));
-    LAUNCH(h, KID_NCCL, st, launch_signal(px, P2P_KEYS, st));
-    LAUNCH(h, KID_NCCL, st, launch_wait(px, P2P_KEYS, h->err_dev, st));
     // owner side: stable W-way merge of the received runs, overlapped with the gather-push
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
     h->okey = h->ok0;
     h->opay = h->ov0;
-    LAUNCH(h, KID_SORT_PASS, h->side,
-           launch_merge_runs(h->recv_keys, h->rt->recv_counts, W, cap, h->okey, h->opay, h->err_dev, h->side));
+    LAUNCH(h, KID_MERGE, h->side,
+           launch_merge_runs(h->recv_keys, h->rt->recv_counts, W, cap, h->okey, h->opay, h->err_dev, &px, h->side));
+    // X2 fused with the gather (waits for KEYS in its prologue, its last block raises ROWS)
     LAUNCH(h, KID_OWNER_GATHER, st,
            launch_gather_push(px, h->w, h->recv_keys, h->D, cap, h->rows_local, h->err_dev, st));
-    LAUNCH(h, KID_NCCL, st, launch_signal(px, P2P_ROWS, st));
-    LAUNCH(h, KID_NCCL, st, launch_wait(px, P2P_ROWS, h->err_dev, st));
+    pa.wait_kind = P2P_ROWS;  // the pool waits for every owner's rows in its prologue
+    pa.p2p = px;
     pa.rows_src = h->uniq_rows;
     pa.nrows_src = h->max_ids;
     pa.row_idx = h->inv;
@@ -788,7 +792,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     h->opay = h->ov0;
     LAUNCH(h, KID_SORT_PASS, h->side,
            launch_merge_runs(h->recv_keys, h->d_counts + EMB_MAX_WORLD, W, h->n_recv, h->okey, h->opay, h->err_dev,
-                             h->side));
+                             nullptr, h->side));
   } else {
     e = radix_sort_pairs(h->sws, h->recv_keys, nullptr, h->ok0, h->ov0, h->ok1, h->ov1, h->n_recv, h->owner_key_bits,
                          h->side, &h->okey, &h->opay, &nl, prof_hook, h);
@@ -820,6 +824,8 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
   h->last_stream = st;
   const bool mean = h->pool == EMB_POOL_MEAN;
   GradArgs g{};
+  g.wait_kind = -1;
+  g.signal_kind = -1;
   g.dim = h->D;
   g.dy = d_out;
   g.drow = h->drow;
@@ -864,9 +870,11 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
     g.useg = h->outidx;
     g.nout = h->max_ids;
     g.p2p = px;
-    LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
-    LAUNCH(h, KID_NCCL, st, launch_signal(px, P2P_GRADS, st));
-    LAUNCH(h, KID_NCCL, st, launch_wait(px, P2P_GRADS, h->err_dev, st));
+    g.signal_kind = P2P_GRADS;  // the last warp of the requester grad raises GRADS
+    if (g.n > 0)
+      LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
+    else
+      LAUNCH(h, KID_NCCL, st, launch_signal(px, P2P_GRADS, st));
     // owner: merge the W sources' gradients per row (source-rank order) and apply
     GradArgs o = g;
     o.skey = h->okey;
@@ -879,6 +887,8 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
     o.blen = nullptr;
     o.sink_mode = 0;
     o.lmask = 0xFFFFFFFFu;
+    o.signal_kind = -1;
+    o.wait_kind = P2P_GRADS;  // every warp waits for the requesters' gradients in its prologue
     LAUNCH(h, KID_GRAD_APPLY, st, launch_grad(o, st));
     h->state = 0;
     return EMB_OK;

@@ -34,6 +34,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "vec.cuh"
+#include "p2p_dev.cuh"
 
 namespace emb {
 
@@ -116,6 +117,19 @@ __device__ __forceinline__ float *out_row(const GradArgs &a, uint32_t ui, int D)
     return a.p2p.peer_grecv[d] + (size_t)(rt->dst_off[d] + ((int64_t)ui - rt->soff[d])) * D;
   } else {
     return a.out_rows + (size_t)ui * D;
+  }
+}
+
+// the last warp of the grid to finish raises the exchange flag (after every warp fenced its stores)
+__device__ __forceinline__ void grad_signal_last_warp(const GradArgs &a, int64_t nwarps) {
+  __threadfence_system();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    const uint32_t t = atomicAdd(a.p2p.done + a.signal_kind, 1u);
+    if (t == (uint32_t)nwarps - 1) {
+      a.p2p.done[a.signal_kind] = 0;
+      p2p_raise(a.p2p, a.signal_kind);
+    }
   }
 }
 
@@ -230,11 +244,18 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
   const uint32_t wbase = smem_u32(smem) + (uint32_t)(wib * NS * stage_floats * 4);
   const int64_t gw = ((int64_t)blockIdx.x * (blockDim.x >> 5)) + wib;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  if (a.wait_kind >= 0) {  // gradients pushed by the requesters (lane 0 of every warp waits)
+    if (lane == 0) p2p_spin(a.p2p, a.wait_kind, a.err);
+    __syncwarp();
+  }
   const int64_t n = a.n_dev ? *a.n_dev : a.n;
   const int64_t R = (n + nwarps - 1) / nwarps;
   const int64_t p_lo = gw * R;
   const int64_t p_hi = (p_lo + R < n) ? p_lo + R : n;
-  if (p_lo >= p_hi) return;
+  if (p_lo >= p_hi) {
+    if (a.signal_kind >= 0) grad_signal_last_warp(a, nwarps);
+    return;
+  }
   const float *src_base = a.src_mode == 0 ? a.dy : a.src;
   const OptConst oc = opt_const(a);
 
@@ -420,6 +441,7 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
   cp_async_wait<0>();
   if (open) span_piece<CPL, MODE>(a, acc, begins ? 2 * gw + 1 : 2 * gw, open_pos, open_key, R, n);  // continues past the range
   if (MODE == 3) __threadfence_system();  // peer stores of this thread precede the GRADS flag
+  if (a.signal_kind >= 0) grad_signal_last_warp(a, nwarps);
 }
 
 static int g_sms = 0;

@@ -12,101 +12,75 @@
 //                      rank's row buffer, in that rank's send order (gather fused with the exchange);
 //   X3  (grad.cu MODE 3): the requester's merged per-key gradient rows are stored straight into the
 //                      owner's gradient buffer.
-// Ordering: writers fence at system scope (__threadfence_system) before k_signal raises the
-// per-(kind, source) epoch flag in every peer; readers spin on the flags (with a timeout that sets
-// EMB_DEVERR_TIMEOUT instead of hanging) before the consuming kernel runs on the same stream.
+// Ordering: writers fence at system scope (__threadfence_system); the last block (or warp) of the
+// producing kernel then raises the per-(kind, source) epoch flag in every peer; consuming kernels
+// spin on the flags in their prologue (bounded: a timeout sets EMB_DEVERR_TIMEOUT instead of hanging)
+// — no separate signal / wait launches on the critical path (p2p_dev.cuh).
 #include "../../include/emb.h"
 #include "common.cuh"
 #include "internal.h"
+#include "p2p_dev.cuh"
 
 namespace emb {
 
-__device__ __forceinline__ void st_sys_u64(uint64_t *p, uint64_t v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_acq_sys_u64(const uint64_t *p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// X0: write my per-owner counts into row `rank` of every rank's matrix, then raise the COUNTS flag
-__global__ void k_xcounts(P2PArgs a, const int64_t *send_counts) {
+// X0: write my per-owner counts into row `rank` of every rank's matrix, raise the COUNTS flag, wait
+// for every peer's row, then build the route table (one block; everything after reads it)
+__global__ void k_xcounts(P2PArgs a, const int64_t *send_counts, uint32_t *err) {
   const int t = threadIdx.x;  // t = p * W + d
   const int W = a.world;
   if (t < W * W) {
     const int p = t / W, d = t % W;
-    int64_t *m = a.peer_xmat[p];
-    m[a.rank * W + d] = send_counts[d];
+    a.peer_xmat[p][a.rank * W + d] = send_counts[d];
   }
   __syncthreads();
   if (t == 0) {
-    __threadfence_system();
-    for (int p = 0; p < W; ++p) st_sys_u64(a.peer_flags[p] + P2P_COUNTS * EMB_MAX_WORLD + a.rank, a.epoch);
+    p2p_raise(a, P2P_COUNTS);
+    p2p_spin(a, P2P_COUNTS, err);
+    RouteTable *rt = a.rt;
+    const int64_t *m = a.xmat;  // own replica, [src][dst]
+    const int r = a.rank;
+    int64_t s = 0;
+    for (int d = 0; d < W; ++d) {
+      rt->soff[d] = s;
+      s += m[r * W + d];
+    }
+    rt->soff[W] = s;
+    s = 0;
+    for (int q = 0; q < W; ++q) {
+      rt->roff[q] = s;
+      s += m[q * W + r];
+    }
+    rt->roff[W] = s;
+    for (int d = 0; d < W; ++d) {  // where my keys start in owner d's buffer
+      int64_t o = 0;
+      for (int q = 0; q < r; ++q) o += m[q * W + d];
+      rt->dst_off[d] = o;
+    }
+    for (int q = 0; q < W; ++q) {  // where requester q expects my rows (its send offset for owner r)
+      int64_t o = 0;
+      for (int d = 0; d < r; ++d) o += m[q * W + d];
+      rt->src_off[q] = o;
+    }
+    for (int q = 0; q < W; ++q) rt->recv_counts[q] = m[q * W + r];
+    rt->n_recv = rt->roff[W];
+    rt->n_send = rt->soff[W];
   }
 }
-cudaError_t launch_xcounts(const P2PArgs &a, const int64_t *send_counts, cudaStream_t st) {
-  k_xcounts<<<1, 256, 0, st>>>(a, send_counts);
+cudaError_t launch_xcounts(const P2PArgs &a, const int64_t *send_counts, uint32_t *err, cudaStream_t st) {
+  k_xcounts<<<1, 256, 0, st>>>(a, send_counts, err);
   return cudaGetLastError();
 }
 
 // raise flag `kind` for this rank in every peer (after the previous kernels' peer stores)
-__global__ void k_signal(P2PArgs a, int kind) {
-  __threadfence_system();
-  for (int p = 0; p < a.world; ++p) st_sys_u64(a.peer_flags[p] + kind * EMB_MAX_WORLD + a.rank, a.epoch);
-}
+__global__ void k_signal(P2PArgs a, int kind) { p2p_raise(a, kind); }
 cudaError_t launch_signal(const P2PArgs &a, int kind, cudaStream_t st) {
   k_signal<<<1, 1, 0, st>>>(a, kind);
   return cudaGetLastError();
 }
 
-// wait for flag `kind` from every source; for COUNTS also build the route table
+// wait for flag `kind` from every source
 __global__ void k_wait(P2PArgs a, int kind, uint32_t *err) {
-  const int W = a.world;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < W; ++s) {
-      const uint64_t *f = a.flags + kind * EMB_MAX_WORLD + s;
-      uint64_t spins = 0;
-      while (ld_acq_sys_u64(f) < a.epoch) {
-        __nanosleep(64);
-        if (++spins > (1ull << 26)) {  // ~several seconds: a peer never arrived; do not hang the GPU
-          atomicOr(err, EMB_DEVERR_TIMEOUT);
-          break;
-        }
-      }
-    }
-    __threadfence_system();
-    if (kind == P2P_COUNTS) {
-      RouteTable *rt = a.rt;
-      const int64_t *m = a.xmat;  // own replica, [src][dst]
-      const int r = a.rank;
-      int64_t s = 0;
-      for (int d = 0; d < W; ++d) {
-        rt->soff[d] = s;
-        s += m[r * W + d];
-      }
-      rt->soff[W] = s;
-      s = 0;
-      for (int q = 0; q < W; ++q) {
-        rt->roff[q] = s;
-        s += m[q * W + r];
-      }
-      rt->roff[W] = s;
-      for (int d = 0; d < W; ++d) {  // where my keys start in owner d's buffer
-        int64_t o = 0;
-        for (int q = 0; q < r; ++q) o += m[q * W + d];
-        rt->dst_off[d] = o;
-      }
-      for (int q = 0; q < W; ++q) {  // where requester q expects my rows (its send offset for owner r)
-        int64_t o = 0;
-        for (int d = 0; d < r; ++d) o += m[q * W + d];
-        rt->src_off[q] = o;
-      }
-      for (int q = 0; q < W; ++q) rt->recv_counts[q] = m[q * W + r];
-      rt->n_recv = rt->roff[W];
-      rt->n_send = rt->soff[W];
-    }
-  }
+  if (threadIdx.x == 0) p2p_spin(a, kind, err);
 }
 cudaError_t launch_wait(const P2PArgs &a, int kind, uint32_t *err, cudaStream_t st) {
   k_wait<<<1, 32, 0, st>>>(a, kind, err);
@@ -128,7 +102,7 @@ __global__ void k_push_keys(P2PArgs a, const uint32_t *__restrict__ send_keys) {
     const int d = seg_of(rt->soff, W, q);
     a.peer_recv_keys[d][rt->dst_off[d] + (q - rt->soff[d])] = send_keys[q];
   }
-  __threadfence_system();
+  p2p_signal_last_block(a, P2P_KEYS);
 }
 cudaError_t launch_push_keys(const P2PArgs &a, const uint32_t *send_keys, int64_t cap, cudaStream_t st) {
   int64_t blocks = (cap + 255) / 256;
@@ -142,6 +116,7 @@ cudaError_t launch_push_keys(const P2PArgs &a, const uint32_t *send_keys, int64_
 // row buffer at s's send position (src_off[s] + q). One float4 per thread, a row per D/4 threads.
 __global__ void k_gather_push(P2PArgs a, const float4 *__restrict__ w, const uint32_t *__restrict__ recv_keys,
                               int d4, int64_t rows_local, uint32_t *err) {
+  p2p_wait_block(a, P2P_KEYS, err);
   const RouteTable *rt = a.rt;
   const int W = a.world;
   const int64_t n = rt->n_recv * d4;
@@ -158,7 +133,7 @@ __global__ void k_gather_push(P2PArgs a, const float4 *__restrict__ w, const uin
     float4 *dst = reinterpret_cast<float4 *>(a.peer_uniq_rows[s]) + (size_t)(rt->src_off[s] + (i - rt->roff[s])) * d4 + c;
     *dst = v;
   }
-  __threadfence_system();
+  p2p_signal_last_block(a, P2P_ROWS);
 }
 cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t *recv_keys, int dim, int64_t cap,
                                int64_t rows_local, uint32_t *err, cudaStream_t st) {
