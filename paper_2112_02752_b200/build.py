@@ -12,6 +12,7 @@ from __future__ import annotations
 import argparse
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -53,25 +54,44 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(ROOT, "include", "emb.h")]
-    newest_hdr = max(os.path.getmtime(h) for h in hdrs)
     flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
              "-I", os.path.join(ROOT, "include"), "-I", inc] + ARCH
+    # an object is reused only if the hash of (its source, every header, the flags) matches the stamp
+    # written when it was compiled: file copies (snapshots to the GPU box) do not keep mtimes
+    hh = hashlib.sha256(" ".join(flags).encode())
+    for h in sorted(hdrs):
+        hh.update(open(h, "rb").read())
     jobs = []
     objs = []
+    stamps = {}
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
-        if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), newest_hdr):
-            jobs.append([NVCC] + flags + ["-c", s, "-o", o])
+        d = hh.copy()
+        d.update(open(s, "rb").read())
+        stamps[o] = d.hexdigest()
+        st = o + ".sha"
+        if force or not os.path.exists(o) or not os.path.exists(st) or open(st).read() != stamps[o]:
+            jobs.append(([NVCC] + flags + ["-c", s, "-o", o], o))
     logs = []
     if jobs:
+        for o in [o for _, o in jobs]:
+            if os.path.exists(o + ".sha"):
+                os.remove(o + ".sha")
         with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
-            logs = list(ex.map(_run, jobs))
+            logs = list(ex.map(_run, [c for c, _ in jobs]))
+        for _, o in jobs:
+            with open(o + ".sha", "w") as f:
+                f.write(stamps[o])
         with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
             f.write("\n".join(logs))
-    if jobs or not os.path.exists(LIB):
+    link_stamp = hashlib.sha256("".join(stamps[o] for o in objs).encode()).hexdigest()
+    lst = LIB + ".sha"
+    if jobs or not os.path.exists(LIB) or not os.path.exists(lst) or open(lst).read() != link_stamp:
         _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
              ["-L", libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath," + libdir, "-lcudart"])
+        with open(lst, "w") as f:
+            f.write(link_stamp)
     if verbose:
         print(LIB)
     return LIB

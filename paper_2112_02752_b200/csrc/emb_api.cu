@@ -611,7 +611,6 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   if (batch > 0 && !direct) LAUNCH(h, KID_KEYS, st, launch_keys(ka, st));
 
   PoolArgs pa{};
-  pa.wait_kind = -1;
   pa.key = h->key_csr;
   pa.offsets = offsets;
   pa.nnz = nnz;
@@ -729,18 +728,20 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     // X0 (counts + wait + route table), X1 (keys; its last block raises KEYS)
     LAUNCH(h, KID_NCCL, st, launch_xcounts(px, h->d_counts, h->err_dev, st));
     LAUNCH(h, KID_ROUTE, st, launch_push_keys(px, h->send_keys, nnz, st));
+    // consumers wait in a one-thread kernel, not in their own prologue: a spinning grid would hold
+    // SMs the concurrent side-stream merge and the gather need (measured slower at W = 4)
+    LAUNCH(h, KID_WAIT, st, launch_wait(px, P2P_KEYS, h->err_dev, st));
     // owner side: stable W-way merge of the received runs, overlapped with the gather-push
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
     h->okey = h->ok0;
     h->opay = h->ov0;
     LAUNCH(h, KID_MERGE, h->side,
-           launch_merge_runs(h->recv_keys, h->rt->recv_counts, W, cap, h->okey, h->opay, h->err_dev, &px, h->side));
-    // X2 fused with the gather (waits for KEYS in its prologue, its last block raises ROWS)
+           launch_merge_runs(h->recv_keys, h->rt->recv_counts, W, cap, h->okey, h->opay, h->err_dev, h->side));
+    // X2 fused with the gather (its last block raises ROWS)
     LAUNCH(h, KID_OWNER_GATHER, st,
            launch_gather_push(px, h->w, h->recv_keys, h->D, cap, h->rows_local, h->err_dev, st));
-    pa.wait_kind = P2P_ROWS;  // the pool waits for every owner's rows in its prologue
-    pa.p2p = px;
+    LAUNCH(h, KID_WAIT, st, launch_wait(px, P2P_ROWS, h->err_dev, st));
     pa.rows_src = h->uniq_rows;
     pa.nrows_src = h->max_ids;
     pa.row_idx = h->inv;
@@ -792,7 +793,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     h->opay = h->ov0;
     LAUNCH(h, KID_SORT_PASS, h->side,
            launch_merge_runs(h->recv_keys, h->d_counts + EMB_MAX_WORLD, W, h->n_recv, h->okey, h->opay, h->err_dev,
-                             nullptr, h->side));
+                             h->side));
   } else {
     e = radix_sort_pairs(h->sws, h->recv_keys, nullptr, h->ok0, h->ov0, h->ok1, h->ov1, h->n_recv, h->owner_key_bits,
                          h->side, &h->okey, &h->opay, &nl, prof_hook, h);
@@ -824,7 +825,6 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
   h->last_stream = st;
   const bool mean = h->pool == EMB_POOL_MEAN;
   GradArgs g{};
-  g.wait_kind = -1;
   g.signal_kind = -1;
   g.dim = h->D;
   g.dy = d_out;
@@ -888,7 +888,7 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
     o.sink_mode = 0;
     o.lmask = 0xFFFFFFFFu;
     o.signal_kind = -1;
-    o.wait_kind = P2P_GRADS;  // every warp waits for the requesters' gradients in its prologue
+    LAUNCH(h, KID_WAIT, st, launch_wait(px, P2P_GRADS, h->err_dev, st));
     LAUNCH(h, KID_GRAD_APPLY, st, launch_grad(o, st));
     h->state = 0;
     return EMB_OK;

@@ -244,10 +244,6 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
   const uint32_t wbase = smem_u32(smem) + (uint32_t)(wib * NS * stage_floats * 4);
   const int64_t gw = ((int64_t)blockIdx.x * (blockDim.x >> 5)) + wib;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  if (a.wait_kind >= 0) {  // gradients pushed by the requesters (lane 0 of every warp waits)
-    if (lane == 0) p2p_spin(a.p2p, a.wait_kind, a.err);
-    __syncwarp();
-  }
   const int64_t n = a.n_dev ? *a.n_dev : a.n;
   const int64_t R = (n + nwarps - 1) / nwarps;
   const int64_t p_lo = gw * R;

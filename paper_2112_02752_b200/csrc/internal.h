@@ -79,8 +79,8 @@ struct P2PArgs {
   float *peer_grecv[P2P_MAXW];
 };
 cudaError_t launch_xcounts(const P2PArgs &a, const int64_t *send_counts, uint32_t *err, cudaStream_t st);
-// device helpers (p2p_dev.cuh) are used inside pool / grad / merge kernels to fold the waits and
-// signals of the exchange into the kernels that consume / produce the data
+// device helpers (p2p_dev.cuh): the producing kernels (push_keys, gather_push, grad MODE 3) raise
+// their exchange flag from their last block / warp
 cudaError_t launch_signal(const P2PArgs &a, int kind, cudaStream_t st);
 cudaError_t launch_wait(const P2PArgs &a, int kind, uint32_t *err, cudaStream_t st);
 cudaError_t launch_push_keys(const P2PArgs &a, const uint32_t *send_keys, int64_t cap, cudaStream_t st);
@@ -143,8 +143,6 @@ struct PoolArgs {
   float *out;
   uint32_t *err;           // device error word (copied to err_host by block 0)
   uint32_t *err_host;      // mapped pinned host word (may be null)
-  int32_t wait_kind;       // >= 0: wait for this p2p flag from every peer before reading rows_src
-  P2PArgs p2p;
 };
 cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st);
 cudaError_t launch_publish_err(const uint32_t *err, uint32_t *err_host, cudaStream_t st);
@@ -168,9 +166,8 @@ struct GradArgs {
   // owner's gradient buffer through peer memory (p2p exchange)
   int32_t sink_mode;
   const int64_t *n_dev;    // if set, the number of sorted positions is read from the device
-  int32_t wait_kind;       // >= 0: wait for this p2p flag from every peer before reading src rows
   int32_t signal_kind;     // >= 0: the last warp to finish raises this p2p flag in every peer
-  P2PArgs p2p;             // sink mode 2 / waits / signals
+  P2PArgs p2p;             // sink mode 2 / signal
   uint32_t lmask;
   int32_t opt;             // 0 sgd 1 adagrad
   double lr, eps;
@@ -242,7 +239,7 @@ cudaError_t launch_partition(const uint32_t *ukey, const uint32_t *u_count, int6
 cudaError_t launch_outidx(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, const uint32_t *sp,
                           int64_t n, uint32_t *outidx, uint32_t *inv, cudaStream_t st);
 cudaError_t launch_merge_runs(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t n, uint32_t *okey,
-                              uint32_t *opay, uint32_t *err, const P2PArgs *wait, cudaStream_t st);
+                              uint32_t *opay, uint32_t *err, cudaStream_t st);
 cudaError_t launch_owner_gather(const float *w, const uint32_t *local, int64_t n, int32_t dim, float *out,
                                 cudaStream_t st);
 

@@ -4,7 +4,7 @@
 // Every rank maps its peers' receive buffers (CUDA IPC, handles all-gathered once over NCCL at
 // create). One step, no host synchronisation:
 //   X0  k_xcounts    : my per-owner key counts -> row `rank` of EVERY rank's W x W count matrix;
-//       k_wait       : spin (bounded) until all W rows arrived, then build the route table (send /
+//                      spin (bounded) until all W rows arrived, then build the route table (send /
 //                      receive offsets, where my keys land in each owner, where rows land in each
 //                      requester);
 //   X1  k_push_keys  : my distinct keys (local ids) stored straight into each owner's key buffer;
@@ -13,9 +13,11 @@
 //   X3  (grad.cu MODE 3): the requester's merged per-key gradient rows are stored straight into the
 //                      owner's gradient buffer.
 // Ordering: writers fence at system scope (__threadfence_system); the last block (or warp) of the
-// producing kernel then raises the per-(kind, source) epoch flag in every peer; consuming kernels
-// spin on the flags in their prologue (bounded: a timeout sets EMB_DEVERR_TIMEOUT instead of hanging)
-// — no separate signal / wait launches on the critical path (p2p_dev.cuh).
+// producing kernel then raises the per-(kind, source) epoch flag in every peer (p2p_dev.cuh); a
+// one-thread k_wait spins on the flags (bounded: a timeout sets EMB_DEVERR_TIMEOUT instead of
+// hanging) before the consuming kernel runs on the same stream. Waiting inside the consumers'
+// prologues instead was measured slower at W = 4 (spinning grids hold SMs the side-stream merge and
+// the gather need).
 #include "../../include/emb.h"
 #include "common.cuh"
 #include "internal.h"
@@ -116,7 +118,6 @@ cudaError_t launch_push_keys(const P2PArgs &a, const uint32_t *send_keys, int64_
 // row buffer at s's send position (src_off[s] + q). One float4 per thread, a row per D/4 threads.
 __global__ void k_gather_push(P2PArgs a, const float4 *__restrict__ w, const uint32_t *__restrict__ recv_keys,
                               int d4, int64_t rows_local, uint32_t *err) {
-  p2p_wait_block(a, P2P_KEYS, err);
   const RouteTable *rt = a.rt;
   const int W = a.world;
   const int64_t n = rt->n_recv * d4;

@@ -36,12 +36,6 @@ __device__ __forceinline__ void p2p_raise(const P2PArgs &a, int kind) {
   for (int p = 0; p < a.world; ++p) st_sys_u64(a.peer_flags[p] + kind * P2P_MAXW + a.rank, a.epoch);
 }
 
-// block prologue: every block waits (thread 0 spins, the block syncs)
-__device__ __forceinline__ void p2p_wait_block(const P2PArgs &a, int kind, uint32_t *err) {
-  if (threadIdx.x == 0) p2p_spin(a, kind, err);
-  __syncthreads();
-}
-
 // block epilogue: after the block's peer stores, the last block to finish raises flag `kind`
 __device__ __forceinline__ void p2p_signal_last_block(const P2PArgs &a, int kind) {
   __threadfence_system();

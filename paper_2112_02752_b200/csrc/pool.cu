@@ -18,7 +18,6 @@
 #include "common.cuh"
 #include "internal.h"
 #include "vec.cuh"
-#include "p2p_dev.cuh"
 
 namespace emb {
 
@@ -134,7 +133,6 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
   const int64_t ntiles = (nb + 31) / 32;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  if (a.wait_kind >= 0) p2p_wait_block(a.p2p, a.wait_kind, a.err);  // rows pushed by the owners
   for (int64_t tile = gw; tile < ntiles; tile += nwarps) {
     const int64_t b0 = tile * 32;
     const int nbt = (int)((nb - b0) < 32 ? (nb - b0) : 32);

@@ -14,7 +14,6 @@
 #include "../../include/emb.h"
 #include "common.cuh"
 #include "internal.h"
-#include "p2p_dev.cuh"
 
 namespace emb {
 
@@ -149,9 +148,8 @@ cudaError_t launch_outidx(const uint32_t *skey, const uint32_t *spay, const uint
 // owner side: stable W-way merge of the received runs (counts in recv_counts[0..W))
 __global__ void k_merge_runs(const uint32_t *__restrict__ rkeys, const int64_t *__restrict__ recv_counts, int W,
                              int64_t cap, uint32_t *__restrict__ okey, uint32_t *__restrict__ opay,
-                             uint32_t *err, P2PArgs pw, int do_wait) {
+                             uint32_t *err) {
   __shared__ int64_t start[EMB_MAX_WORLD + 1];
-  if (do_wait) p2p_wait_block(pw, P2P_KEYS, err);  // the keys arrive from the peers
   if (threadIdx.x == 0) {
     start[0] = 0;
     for (int r = 0; r < W; ++r) start[r + 1] = start[r] + recv_counts[r];
@@ -185,13 +183,10 @@ __global__ void k_merge_runs(const uint32_t *__restrict__ rkeys, const int64_t *
   }
 }
 cudaError_t launch_merge_runs(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t n, uint32_t *okey,
-                              uint32_t *opay, uint32_t *err, const P2PArgs *wait, cudaStream_t st) {
+                              uint32_t *opay, uint32_t *err, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t blocks = (n + 255) / 256;
-  P2PArgs pw{};
-  if (wait) pw = *wait;
-  k_merge_runs<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(rkeys, recv_counts, W, n, okey, opay, err,
-                                                                          pw, wait != nullptr);
+  k_merge_runs<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(rkeys, recv_counts, W, n, okey, opay, err);
   return cudaGetLastError();
 }
 
