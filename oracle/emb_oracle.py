@@ -19,8 +19,9 @@ R1-R22 of SURVEY.md §8(c), restated in DESIGN.md §3):
   6. backward  c_j = dY[b, s, :] (sum) or dY[b, s, :] / |bag| (mean);  G[g] = sum_j c_j in fp64 over all
                ranks (no 1/B, no 1/W)                                                     (R8-R11)
   7. update    SGD: w <- w - lr*G ;  Adagrad (element-wise, eps outside sqrt): a <- a + G^2,
-               w <- w - lr*G/(sqrt(a)+eps); computed in fp64 from the fp32 state, rounded once;
-               untouched rows bitwise unchanged                                           (R12-R14)
+               w <- w - lr*G/(sqrt(a)+eps); row-wise Adagrad (one accumulator per row, SURVEY
+               §8(f) f1): a_r <- a_r + mean_c(G[c]^2), w <- w - lr*G/(sqrt(a_r)+eps); computed in
+               fp64 from the fp32 state, rounded once; untouched rows bitwise unchanged   (R12-R14')
   8. init      w[g, c] = int16(splitmix64(seed XOR (g*D + c)) >> 48) * 2^-19,  a = init_accum  (R15)
 
 Everything is the plain definition written out with NumPy primitives (np.unique, np.add.at,
@@ -69,7 +70,7 @@ class OracleConfig:
     dim: int
     slot_table: Tuple[int, ...]    # slot -> table
     pool: str = "sum"              # "sum" | "mean"
-    opt: str = "adagrad"           # "sgd" | "adagrad"
+    opt: str = "adagrad"           # "sgd" | "adagrad" | "rowwise_adagrad"
     eps: float = 1e-6
     init_accum: float = 0.0
     seed: int = 2112
@@ -87,6 +88,12 @@ class OracleConfig:
     @property
     def total_rows(self) -> int:
         return int(sum(self.rows))
+
+    @property
+    def accum_width(self) -> int:
+        """Optimizer state floats per row: D (element-wise Adagrad, and the unused SGD slot) or 1
+        (row-wise Adagrad, R14')."""
+        return 1 if self.opt == "rowwise_adagrad" else self.dim
 
 
 def config_from_workload(wl, world: int = 1, shard: str = "cyclic") -> OracleConfig:
@@ -177,7 +184,7 @@ class SparseState:
         self.cfg = cfg
         self.keys = np.zeros(0, dtype=np.int64)
         self.w = np.zeros((0, cfg.dim), dtype=np.float32)
-        self.a = np.zeros((0, cfg.dim), dtype=np.float32)
+        self.a = np.zeros((0, cfg.accum_width), dtype=np.float32)
 
     def _find(self, g):
         pos = np.searchsorted(self.keys, g)
@@ -188,7 +195,7 @@ class SparseState:
     def get(self, g: np.ndarray):
         g = np.asarray(g, dtype=np.int64).reshape(-1)
         w = init_weights(self.cfg.seed, g, self.cfg.dim)
-        a = np.full((g.size, self.cfg.dim), self.cfg.init_accum, dtype=np.float32)
+        a = np.full((g.size, self.cfg.accum_width), self.cfg.init_accum, dtype=np.float32)
         if self.keys.size and g.size:
             pos, hit = self._find(g)
             w[hit] = self.w[pos[hit]]
@@ -265,10 +272,21 @@ def adagrad_update(w: np.ndarray, a: np.ndarray, G: np.ndarray, lr: float, eps: 
     return w64.astype(np.float32), a64.astype(np.float32)
 
 
+def rowwise_adagrad_update(w: np.ndarray, a: np.ndarray, G: np.ndarray, lr: float, eps: float):
+    """Row-wise Adagrad (reading R14'): one accumulator per row, a [U, 1]:
+    a <- a + (1/D) sum_c G[c]^2;  w <- w - lr*G/(sqrt(a)+eps); fp64, one rounding each."""
+    a64 = a.astype(np.float64) + np.mean(G * G, axis=1, keepdims=True)
+    w64 = w.astype(np.float64) - lr * G / (np.sqrt(a64) + eps)
+    return w64.astype(np.float32), a64.astype(np.float32)
+
+
 def apply_update(cfg: OracleConfig, state: SparseState, U: np.ndarray, G: np.ndarray, lr: float):
     w, a = state.get(U)
     if cfg.opt == "sgd":
         state.set(U, sgd_update(w, G, lr), a)
+    elif cfg.opt == "rowwise_adagrad":
+        w2, a2 = rowwise_adagrad_update(w, a, G, lr, cfg.eps)
+        state.set(U, w2, a2)
     else:
         w2, a2 = adagrad_update(w, a, G, lr, cfg.eps)
         state.set(U, w2, a2)

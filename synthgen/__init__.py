@@ -41,7 +41,7 @@ class Workload:
     ids: str                        # "uniform" | "zipf" | "hot1k"
     zipf_s: float = 1.05
     pool: str = "sum"               # "sum" | "mean"
-    opt: str = "adagrad"            # "sgd" | "adagrad"
+    opt: str = "adagrad"            # "sgd" | "adagrad" | "rowwise_adagrad"
     lr: float = 0.01
     eps: float = 1e-6               # R13
     init_accum: float = 0.0         # R13

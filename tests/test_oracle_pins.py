@@ -118,6 +118,57 @@ def test_adagrad_hand_worked():
         assert w[0, 0] == np.float32(st["w"])
 
 
+def test_rowwise_adagrad_hand_worked():
+    # SURVEY §8(f) f1 / reading R14': hand-worked fixture (exact binary-fraction inputs)
+    d = _gold("rowwise_adagrad_hand.json")
+    cfg = O.OracleConfig(rows=(1,), dim=2, slot_table=(0,), pool="sum", opt="rowwise_adagrad", eps=d["eps"])
+    emb = O.OracleEmbedding(cfg)
+    emb.load_rows(np.array([0]), np.array([d["w0"]], np.float32), np.array([[d["a0"]]], np.float32))
+    for st in d["steps"]:
+        occ = st["occurrences"]
+        ids = np.zeros(len(occ), dtype=np.int64)
+        offs = np.arange(len(occ) + 1)
+        emb.lookup([(ids, offs, len(occ))])
+        dy = np.array(occ, dtype=np.float32).reshape(len(occ), 1, 2)
+        emb.backward_update([dy], d["lr"])
+        w, a = emb.rows(np.array([0]))
+        assert a.shape == (1, 1)
+        assert a[0, 0] == np.float32(st["a"])
+        assert np.array_equal(w[0], np.array(st["w_fp64"], dtype=np.float32))
+
+
+def test_rowwise_adagrad_reduces_to_elementwise():
+    # special cases that reduce to the (torch-pinned) element-wise Adagrad: D = 1, and a gradient whose
+    # columns are all equal (mean_c G^2 = G^2 in every column) with equal initial accumulators
+    rng = np.random.default_rng(5)
+    for D, equal_cols in ((1, False), (8, True)):
+        U = 50
+        w = rng.standard_normal((U, D)).astype(np.float32)
+        a0 = rng.uniform(0, 2, (U, 1)).astype(np.float32)
+        G = rng.standard_normal((U, 1 if equal_cols else D)) * np.ones((1, D))
+        w_r, a_r = O.rowwise_adagrad_update(w, a0, G, 0.05, 1e-6)
+        w_e, a_e = O.adagrad_update(w, np.repeat(a0, D, axis=1), G, 0.05, 1e-6)
+        assert np.array_equal(w_r, w_e)
+        assert np.array_equal(np.repeat(a_r, D, axis=1), a_e)
+
+
+def test_rowwise_adagrad_state_is_per_row_and_monotone():
+    cfg = O.OracleConfig(rows=(40,), dim=4, slot_table=(0,), opt="rowwise_adagrad", init_accum=0.1)
+    emb = O.OracleEmbedding(cfg)
+    ids = np.array([3, 3, 7, 11], dtype=np.int64)
+    offs = np.array([0, 2, 3, 4])
+    prev = emb.rows(np.array([3, 7, 11, 20]))[1]
+    assert prev.shape == (4, 1) and np.all(prev == np.float32(0.1))
+    emb.lookup([(ids, offs, 3)])
+    emb.backward_update([np.ones((3, 1, 4), np.float32)], 0.01)
+    w, a = emb.rows(np.array([3, 7, 11, 20]))
+    # row 3: two occurrences of an all-ones dY -> G = 2 in every column -> a = 0.1 + 4
+    assert a[0, 0] == np.float32(np.float64(np.float32(0.1)) + 4.0)
+    assert a[1, 0] == a[2, 0] == np.float32(np.float64(np.float32(0.1)) + 1.0)
+    assert a[3, 0] == np.float32(0.1)  # untouched
+    assert np.array_equal(w[3], O.init_weights(cfg.seed, np.array([20]), 4)[0])
+
+
 # ----------------------------------------------------------------------------- dense one-hot matmul
 def _onehot(cfg, ids, offs, B, s):
     """A_s[b, id] = multiplicity of id in bag (s, b) — built by a plain Python loop (brute force)."""
