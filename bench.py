@@ -68,19 +68,27 @@ def describe(wl, n):
 def step_bytes(wl, N, SB, U_l, U_o, W):
     """HBM bytes the method must move per GPU per step."""
     D = wl.dim
-    k = 16 if wl.opt == "adagrad" else 8
     fwd = 8 * N + 8 * (SB + 1) + 4 * D * U_o + 4 * D * SB
-    bwd = 4 * D * SB + 8 * N + 8 * (SB + 1) + k * D * U_o
+    bwd = 4 * D * SB + 8 * N + 8 * (SB + 1) + state_bytes(wl, U_o)
     return fwd + bwd
+
+
+def state_bytes(wl, U):
+    """Optimizer read-modify-write per touched row: w (+ a) read and written."""
+    D = wl.dim
+    if wl.opt == "adagrad":
+        return 16 * D * U
+    if wl.opt == "rowwise_adagrad":
+        return (8 * D + 8) * U
+    return 8 * D * U
 
 
 def kernel_bytes(name, wl, N, SB, U, W):
     """Algorithmic bytes of one launch of the named kernel."""
     D = wl.dim
     if name == "grad_apply":
-        k = 16 if wl.opt == "adagrad" else 8
         # dY row per occurrence + sorted key/payload/bag index per occurrence + state RMW per touched row
-        return 4 * D * N + 12 * N + k * D * U
+        return 4 * D * N + 12 * N + state_bytes(wl, U)
     if name == "pool":
         # offsets + routing keys + one table row per distinct key + Y write
         return 8 * (SB + 1) + 4 * N + 4 * D * U + 4 * D * SB
@@ -186,6 +194,8 @@ def main():
     ap.add_argument("--workload", default=None, help="override (C1..C5) for experiments")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--opt", default=None, choices=["sgd", "adagrad", "rowwise_adagrad"],
+                    help="override the optimizer (experiments; BJ:8 is element-wise Adagrad)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -197,6 +207,8 @@ def main():
         wl = synthgen.WORKLOADS[args.workload]
     if args.batch:
         wl = wl.with_(batch=args.batch)
+    if args.opt:
+        wl = wl.with_(opt=args.opt)
 
     if args.impl == "reference":
         if rank != 0:
@@ -360,7 +372,7 @@ def main():
                        "unique_local": U_l, "unique_owner": U_o,
                        "l2": f"inputs larger than L2: {POOL_BATCHES} distinct staged batches cycled "
                              f"({POOL_BATCHES} x {(hb_bytes(host_batches[0], wl)) / 1e6:.0f} MB) + "
-                             f"{layer.rows_local * wl.dim * 4 * (2 if wl.opt == 'adagrad' else 1) / 1e9:.1f} GB table "
+                             f"{layer.rows_local * 4 * (wl.dim + layer.accum_width * (wl.opt != 'sgd')) / 1e9:.1f} GB table "
                              "state per GPU"},
             "lookups_per_s": lookups_s,
             "fwd_ms": fwd_ms,

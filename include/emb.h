@@ -58,7 +58,9 @@ typedef enum {
 } emb_status_t;
 
 typedef enum { EMB_POOL_SUM = 0, EMB_POOL_MEAN = 1 } emb_pool_t;          /* R1 */
-typedef enum { EMB_OPT_SGD = 0, EMB_OPT_ADAGRAD = 1 } emb_opt_t;          /* R12 */
+/* R12; EMB_OPT_ROWWISE_ADAGRAD (reading R14'): one fp32 accumulator per row,
+   a <- a + (1/D) sum_c G[c]^2, w <- w - lr*G/(sqrt(a)+eps) -- 4 bytes of state per row instead of 4D */
+typedef enum { EMB_OPT_SGD = 0, EMB_OPT_ADAGRAD = 1, EMB_OPT_ROWWISE_ADAGRAD = 2 } emb_opt_t;
 typedef enum { EMB_SHARD_CYCLIC = 0, EMB_SHARD_BLOCK = 1 } emb_shard_t;   /* R7 */
 
 typedef struct {
@@ -135,8 +137,9 @@ emb_status_t emb_backward_update_host(emb_handle_t h, const float *d_out, double
 /* ---- host-synchronous helpers (tests, checkpoint, accounting; call between steps) ------------- */
 
 /* Read / overwrite rows of table `table` that THIS rank owns (owner(base[table]+row) == rank, else
- * EMB_ERR_INVALID). rows_host: host int64 [n] table-local ids; w_host, a_host: host fp32 [n][D];
- * a_host may be NULL (ignored for SGD). Synchronises the handle's last stream. */
+ * EMB_ERR_INVALID). rows_host: host int64 [n] table-local ids; w_host: host fp32 [n][D]; a_host: host
+ * fp32 [n][D] (element-wise Adagrad) or [n] (row-wise Adagrad); a_host may be NULL (ignored for SGD).
+ * Synchronises the handle's last stream. */
 emb_status_t emb_read_rows(emb_handle_t h, int32_t table, const int64_t *rows_host, int64_t n,
                            float *w_host, float *a_host);
 emb_status_t emb_write_rows(emb_handle_t h, int32_t table, const int64_t *rows_host, int64_t n,

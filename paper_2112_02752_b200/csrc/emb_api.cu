@@ -224,6 +224,9 @@ int64_t local_of_global(const emb_ctx *h, uint64_t g) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// optimizer-state floats per row: D (element-wise Adagrad) or 1 (row-wise)
+int32_t accum_width(const emb_ctx *h) { return h->opt == EMB_OPT_ROWWISE_ADAGRAD ? 1 : h->D; }
+
 // world > 1: map every peer's exchange buffers (CUDA IPC handles all-gathered over NCCL)
 emb_status_t setup_p2p(emb_ctx *h) {
   const int W = h->world;
@@ -307,7 +310,8 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   if (cfg->dim < 4 || cfg->dim > 256 || cfg->dim % 4 != 0 || (cfg->dim > 128 && cfg->dim % 8 != 0))
     return fail(h, EMB_ERR_INVALID, "dim must be a multiple of 4 in [4, 256] (multiple of 8 above 128)");
   if (cfg->pool != EMB_POOL_SUM && cfg->pool != EMB_POOL_MEAN) return fail(h, EMB_ERR_INVALID, "bad pool");
-  if (cfg->opt != EMB_OPT_SGD && cfg->opt != EMB_OPT_ADAGRAD) return fail(h, EMB_ERR_INVALID, "bad opt");
+  if (cfg->opt != EMB_OPT_SGD && cfg->opt != EMB_OPT_ADAGRAD && cfg->opt != EMB_OPT_ROWWISE_ADAGRAD)
+    return fail(h, EMB_ERR_INVALID, "bad opt");
   if (!(cfg->eps > 0)) return fail(h, EMB_ERR_INVALID, "eps must be > 0");
   if (!(cfg->init_accum >= 0)) return fail(h, EMB_ERR_INVALID, "init_accum must be >= 0");
   if (cfg->max_batch < 1 || cfg->max_ids < 1 || cfg->max_ids >= (1ll << 30))
@@ -385,6 +389,8 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   if (dalloc(h, &h->w, row_elems) != cudaSuccess) return fail(h, EMB_ERR_NOMEM, "cannot allocate the table shard");
   if (h->opt == EMB_OPT_ADAGRAD && dalloc(h, &h->a, row_elems) != cudaSuccess)
     return fail(h, EMB_ERR_NOMEM, "cannot allocate the Adagrad state");
+  if (h->opt == EMB_OPT_ROWWISE_ADAGRAD && dalloc(h, &h->a, (size_t)std::max<int64_t>(h->rows_local, 1)) != cudaSuccess)
+    return fail(h, EMB_ERR_NOMEM, "cannot allocate the row-wise Adagrad state");
   {
     // the side stream carries the latency-critical sort: highest priority, so its CTAs are scheduled
     // ahead of the bandwidth-bound pool CTAs as SMs free up
@@ -394,7 +400,8 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   }
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-  CUDA_TRY(h, launch_init(h->w, h->a, h->rows_local, h->D, h->seed, h->init_accum, ks, h->rank, h->side));
+  CUDA_TRY(h, launch_init(h->w, h->a, h->opt == EMB_OPT_ROWWISE_ADAGRAD, h->rows_local, h->D, h->seed,
+                          h->init_accum, ks, h->rank, h->side));
 
   // small config arrays
   if (dalloc(h, &h->d_slot_table, h->S) || dalloc(h, &h->d_base, h->T) || dalloc(h, &h->d_rows, h->T))
@@ -655,7 +662,10 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
       sa.err = h->err_dev;
       h->skey = h->k0;
       h->spay = h->v0;
-      if (batch > 0) LAUNCH(h, KID_SORT_PASS, h->side, launch_segsort(sa, h->G, h->side));
+      static int serial = -1;  // experiment knob: EMB_SERIAL=1 runs the sort before the pool (no overlap)
+      if (serial < 0) serial = getenv("EMB_SERIAL") ? atoi(getenv("EMB_SERIAL")) : 0;
+      cudaStream_t ss = serial ? st : h->side;
+      if (batch > 0) LAUNCH(h, KID_SORT_PASS, ss, launch_segsort(sa, h->G, ss));
     } else {
       int nl = 0;
       cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz,
@@ -1116,12 +1126,13 @@ emb_status_t emb_read_rows(emb_handle_t h, int32_t table, const int64_t *rows_ho
   cudaError_t e = cudaMemcpy(d_loc, loc.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = launch_rows_gather(h->w, d_loc, n, h->D, d_buf, 0);
   if (e == cudaSuccess) e = cudaMemcpy(w_host, d_buf, sizeof(float) * n * h->D, cudaMemcpyDeviceToHost);
+  const int32_t aw = accum_width(h);
   if (e == cudaSuccess && a_host) {
     if (h->a) {
-      e = launch_rows_gather(h->a, d_loc, n, h->D, d_buf, 0);
-      if (e == cudaSuccess) e = cudaMemcpy(a_host, d_buf, sizeof(float) * n * h->D, cudaMemcpyDeviceToHost);
+      e = launch_rows_gather(h->a, d_loc, n, aw, d_buf, 0);
+      if (e == cudaSuccess) e = cudaMemcpy(a_host, d_buf, sizeof(float) * n * aw, cudaMemcpyDeviceToHost);
     } else {
-      std::fill(a_host, a_host + n * h->D, 0.f);
+      std::fill(a_host, a_host + n * aw, 0.f);
     }
   }
   cudaFree(d_loc);
@@ -1154,9 +1165,10 @@ emb_status_t emb_write_rows(emb_handle_t h, int32_t table, const int64_t *rows_h
   if (e == cudaSuccess) e = cudaMemcpy(d_buf, w_host, sizeof(float) * n * h->D, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = launch_rows_scatter(h->w, d_loc, n, h->D, d_buf, 0);
   if (e == cudaSuccess && a_host && h->a) {
+    const int32_t aw = accum_width(h);
     e = cudaDeviceSynchronize();
-    if (e == cudaSuccess) e = cudaMemcpy(d_buf, a_host, sizeof(float) * n * h->D, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = launch_rows_scatter(h->a, d_loc, n, h->D, d_buf, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(d_buf, a_host, sizeof(float) * n * aw, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_rows_scatter(h->a, d_loc, n, aw, d_buf, 0);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   cudaFree(d_loc);

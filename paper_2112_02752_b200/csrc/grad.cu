@@ -28,7 +28,10 @@
 // (element-wise, eps outside the sqrt, R12): a <- a + G^2 in fp64 rounded to fp32; the update
 // lr*G/(sqrt(a)+eps) in fp32 with MUFU sqrt/rcp (|update| <= lr, so its relative error of a few
 // 1e-7 is <= 1e-8 absolute, far inside the 1e-6 + 1e-5|w| tolerance; DESIGN.md §3 R16').
-// 2 = write the fp32 per-unique-key gradient (requester side of the W>1 exchange).
+// 2 = write the fp32 per-unique-key gradient (requester side of the W>1 exchange). 3 = the same row
+// stored into the owner through peer memory. 4 = row-wise Adagrad (SURVEY §8(f) f1, R14'): one
+// accumulator per row, a <- a + (1/D) sum_c G[c]^2 (fp64 xor-butterfly warp reduction: every lane
+// ends with the same total) rounded to fp32; w as in mode 1 with the row's a.
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -104,6 +107,35 @@ __device__ __forceinline__ void apply_frag(const GradArgs &a, const OptConst &oc
     stg_frag<CPL>(a.w + row_off, wo);
     stg_frag<CPL>(a.a + row_off, ao);
   }
+}
+
+// row-wise Adagrad (MODE 4) of one row: warp-collective (every lane calls it; inactive lanes hold no
+// columns). a_old is the row's accumulator (the same value in every lane).
+template <int CPL>
+__device__ __forceinline__ void apply_rowwise(const GradArgs &a, const OptConst &oc, const double (&acc)[CPL],
+                                              const VecF<CPL> &wv, float a_old, size_t row_off, uint32_t lrow,
+                                              bool active, int D) {
+  double s = 0.0;
+  if (active) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) s = __dadd_rn(s, __dmul_rn(acc[c], acc[c]));
+  }
+  // xor butterfly: at every level the two partners add the same two operands (commutative), so all
+  // lanes end with the bitwise identical total
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  // s / D: a multiply by the exact reciprocal when D is a power of two (every configured D)
+  const double mean = (D & (D - 1)) == 0 ? __dmul_rn(s, 1.0 / (double)D) : __ddiv_rn(s, (double)D);
+  const double a64 = __dadd_rn((double)a_old, mean);
+  const float af = (float)a64;
+  const float r = rcp_approx(sqrt_approx(af) + oc.epsf);
+  if (active) {
+    VecF<CPL> wo;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) wo.v[c] = wv.v[c] - (oc.lrf * (float)acc[c]) * r;
+    stg_frag<CPL>(a.w + row_off, wo);
+  }
+  if ((threadIdx.x & 31) == 0) a.a[lrow] = af;
 }
 
 // destination row of a merged per-key gradient (MODE 2: local X3 send buffer; MODE 3: the owner's
@@ -194,11 +226,12 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
     }
   }
   last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last || !active) return;
+  if (!last) return;
+  if (MODE != 4 && !active) return;  // (row-wise Adagrad reduces over the whole warp)
   double tot[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) tot[c] = 0.0;
-  for (int64_t ww = w0; ww <= w1; ++ww) {
+  for (int64_t ww = w0; ww <= w1 && active; ++ww) {
     const double *src = a.partials + (size_t)(ww == w0 ? 2 * ww + 1 : 2 * ww) * D + col;
 #pragma unroll
     for (int c = 0; c < CPL; c += 2) {
@@ -207,12 +240,20 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
       tot[c + 1] = __dadd_rn(tot[c + 1], v.y);
     }
   }
-  if constexpr (MODE >= 2) {
+  if constexpr (MODE == 2 || MODE == 3) {
     VecF<CPL> o;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) o.v[c] = (float)tot[c];
     stg_frag<CPL>(out_row<MODE>(a, a.useg[pos], D) + col, o);
     if (MODE == 3) __threadfence_system();
+  } else if constexpr (MODE == 4) {
+    const uint32_t lrow = key & a.lmask;
+    const size_t off = (size_t)lrow * D + col;
+    VecF<CPL> wv;
+    if (active) ldg_frag<CPL>(wv, a.w + off);
+    else wv.zero();
+    const float a_old = __ldcg(a.a + lrow);
+    apply_rowwise<CPL>(a, opt_const(a), tot, wv, a_old, off, lrow, active, D);
   } else {
     const size_t off = (size_t)(key & a.lmask) * D + col;
     VecF<CPL> wv, av;
@@ -233,14 +274,14 @@ struct TileMeta {
 template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2>
 __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ GradArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int NA = (MODE == 1) ? 3 : (MODE == 0 ? 2 : 1);  // row arrays per stage: contribution, w, a
-  constexpr bool SINK_OPT = MODE < 2;
+  constexpr int NA = (MODE == 1) ? 3 : ((MODE == 0 || MODE == 4) ? 2 : 1);  // row arrays per stage: contribution, w, a
+  constexpr bool SINK_OPT = MODE < 2 || MODE == 4;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int D = DC ? DC : a.dim;  // compile-time row width for D = 64 / 128 / 256
   const int col = lane * CPL;
   const bool active = DC ? true : col < D;
   const int C16 = D >> 2;  // 16-byte chunks per row (a constant when DC != 0)
-  const size_t stage_floats = (size_t)NA * T * D;
+  const size_t stage_floats = (size_t)NA * T * D + (MODE == 4 ? T : 0);  // (+ T row accumulators)
   const uint32_t wbase = smem_u32(smem) + (uint32_t)(wib * NS * stage_floats * 4);
   const int64_t gw = ((int64_t)blockIdx.x * (blockDim.x >> 5)) + wib;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -324,6 +365,8 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
         if (MODE == 1) cp_async16(sb + (uint32_t)(2 * T * D * 4) + off, a.a + wri + c * 4);
       }
     }
+    if (MODE == 4 && lane < T && ((amask >> lane) & 1u))  // the row's accumulator (4 bytes)
+      cp_async4(sb + (uint32_t)(2 * T * D * 4) + 4u * (uint32_t)lane, a.a + (k & a.lmask));
   };
 
   TileMeta meta[NS];
@@ -395,6 +438,15 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
                 for (int c = 0; c < CPL; ++c) o.v[c] = (float)acc.v[c];
                 stg_frag<CPL>(out_row<MODE>(a, ui, D) + col, o);
               }
+            } else if constexpr (MODE == 4) {
+              VecF<CPL> wv;
+              if (active) lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((T + i) * D));
+              else wv.zero();
+              float a_old;
+              const uint32_t sa_ = wbase + (uint32_t)(s * stage_floats * 4) + 4u * (uint32_t)(2 * T * D + i);
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(a_old) : "r"(sa_));
+              const uint32_t lrow = ki & a.lmask;
+              apply_rowwise<CPL>(a, oc, acc.v, wv, a_old, (size_t)lrow * D + col, lrow, active, D);
             } else {
               if (active) {
                 VecF<CPL> wv, av;
@@ -444,8 +496,8 @@ static int g_sms = 0;
 
 template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2>
 static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
-  constexpr int NA = (MODE == 1) ? 3 : (MODE == 0 ? 2 : 1);
-  const size_t per_warp = (size_t)NS * NA * T * a.dim * sizeof(float);
+  constexpr int NA = (MODE == 1) ? 3 : ((MODE == 0 || MODE == 4) ? 2 : 1);
+  const size_t per_warp = (size_t)NS * ((size_t)NA * T * a.dim + (MODE == 4 ? T : 0)) * sizeof(float);
   int wpc = (int)(110 * 1024 / per_warp);  // warps per CTA: ~110 KB of stages, 2 CTAs per SM
   if (wpc > 8) wpc = 8;
   if (wpc < 1) wpc = 1;
@@ -471,15 +523,17 @@ static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
 template <int CPL, int T, int DC>
 static cudaError_t launch_grad_d(const GradArgs &a, cudaStream_t st) {
   const bool mean = a.blen != nullptr;
-  const int mode = a.sink_mode == 2 ? 3 : (a.sink_mode == 1 ? 2 : (a.opt == 1 ? 1 : 0));
+  const int mode = a.sink_mode == 2 ? 3 : (a.sink_mode == 1 ? 2 : (a.opt == 1 ? 1 : (a.opt == 2 ? 4 : 0)));
   if (mean) {
     if (mode == 0) return launch_grad_t<CPL, T, 2, true, 0, DC>(a, st);
     if (mode == 1) return launch_grad_t<CPL, T, 2, true, 1, DC>(a, st);
+    if (mode == 4) return launch_grad_t<CPL, T, 2, true, 4, DC>(a, st);
     if (mode == 2) return launch_grad_t<CPL, T, 2, true, 2, DC>(a, st);
     return launch_grad_t<CPL, T, 2, true, 3, DC>(a, st);
   }
   if (mode == 0) return launch_grad_t<CPL, T, 2, false, 0, DC>(a, st);
   if (mode == 1) return launch_grad_t<CPL, T, 2, false, 1, DC>(a, st);
+  if (mode == 4) return launch_grad_t<CPL, T, 2, false, 4, DC>(a, st);
   if (mode == 2) return launch_grad_t<CPL, T, 2, false, 2, DC>(a, st);
   return launch_grad_t<CPL, T, 2, false, 3, DC>(a, st);
 }

@@ -169,7 +169,7 @@ struct GradArgs {
   int32_t signal_kind;     // >= 0: the last warp to finish raises this p2p flag in every peer
   P2PArgs p2p;             // sink mode 2 / signal
   uint32_t lmask;
-  int32_t opt;             // 0 sgd 1 adagrad
+  int32_t opt;             // 0 sgd 1 adagrad 2 row-wise adagrad (a: one float per row)
   double lr, eps;
   float *w, *a;
   int64_t nrows;           // rows of w/a (bounds guard)
@@ -200,8 +200,8 @@ size_t unique_status_words(int64_t max_n);
 cudaError_t launch_unique(const UniqueArgs &a, cudaStream_t st);
 
 // table init (R15) and row helpers
-cudaError_t launch_init(float *w, float *a, int64_t rows_local, int32_t dim, uint64_t seed, float init_accum,
-                        const KeySpace &ks, int32_t rank, cudaStream_t st);
+cudaError_t launch_init(float *w, float *a, int32_t a_per_row, int64_t rows_local, int32_t dim, uint64_t seed,
+                        float init_accum, const KeySpace &ks, int32_t rank, cudaStream_t st);
 cudaError_t launch_rows_gather(const float *src, const int64_t *rows, int64_t n, int32_t dim, float *dst,
                                cudaStream_t st);
 cudaError_t launch_rows_scatter(float *dst, const int64_t *rows, int64_t n, int32_t dim, const float *src,

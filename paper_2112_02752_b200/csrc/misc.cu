@@ -174,8 +174,8 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
-__global__ void k_init(float4 *w, float4 *a, int64_t rows_local, int d4, uint64_t seed, float init_accum,
-                       KeySpace ks, int32_t rank) {
+__global__ void k_init(float4 *w, float4 *a, float *a_row, int64_t rows_local, int d4, uint64_t seed,
+                       float init_accum, KeySpace ks, int32_t rank) {
   const int64_t total = rows_local * d4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint64_t D = (uint64_t)d4 * 4;
@@ -194,13 +194,14 @@ __global__ void k_init(float4 *w, float4 *a, int64_t rows_local, int d4, uint64_
     }
     w[t] = make_float4(v[0], v[1], v[2], v[3]);
     if (a) a[t] = make_float4(init_accum, init_accum, init_accum, init_accum);
+    if (a_row && c4 == 0) a_row[r] = init_accum;
   }
 }
-cudaError_t launch_init(float *w, float *a, int64_t rows_local, int32_t dim, uint64_t seed, float init_accum,
-                        const KeySpace &ks, int32_t rank, cudaStream_t st) {
+cudaError_t launch_init(float *w, float *a, int32_t a_per_row, int64_t rows_local, int32_t dim, uint64_t seed,
+                        float init_accum, const KeySpace &ks, int32_t rank, cudaStream_t st) {
   if (rows_local <= 0) return cudaSuccess;
-  k_init<<<148 * 8, 256, 0, st>>>(reinterpret_cast<float4 *>(w), reinterpret_cast<float4 *>(a), rows_local, dim / 4,
-                                  seed, init_accum, ks, rank);
+  k_init<<<148 * 8, 256, 0, st>>>(reinterpret_cast<float4 *>(w), a_per_row ? nullptr : reinterpret_cast<float4 *>(a),
+                                  a_per_row ? a : nullptr, rows_local, dim / 4, seed, init_accum, ks, rank);
   return cudaGetLastError();
 }
 
@@ -212,9 +213,21 @@ __global__ void k_rows_copy(const float4 *src, float4 *dst, const int64_t *rows,
   if (gather) dst[t] = src[(size_t)rows[i] * d4 + c];
   else dst[(size_t)rows[i] * d4 + c] = src[t];
 }
+// one float per row (row-wise Adagrad accumulators)
+__global__ void k_rows_copy1(const float *src, float *dst, const int64_t *rows, int64_t n, int gather) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (gather) dst[i] = src[rows[i]];
+  else dst[rows[i]] = src[i];
+}
+
 cudaError_t launch_rows_gather(const float *src, const int64_t *rows, int64_t n, int32_t dim, float *dst,
                                cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (dim == 1) {
+    k_rows_copy1<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, dst, rows, n, 1);
+    return cudaGetLastError();
+  }
   const int d4 = dim / 4;
   k_rows_copy<<<(unsigned)((n * d4 + 255) / 256), 256, 0, st>>>(reinterpret_cast<const float4 *>(src),
                                                                 reinterpret_cast<float4 *>(dst), rows, n, d4, 1);
@@ -223,6 +236,10 @@ cudaError_t launch_rows_gather(const float *src, const int64_t *rows, int64_t n,
 cudaError_t launch_rows_scatter(float *dst, const int64_t *rows, int64_t n, int32_t dim, const float *src,
                                 cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (dim == 1) {
+    k_rows_copy1<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, dst, rows, n, 0);
+    return cudaGetLastError();
+  }
   const int d4 = dim / 4;
   k_rows_copy<<<(unsigned)((n * d4 + 255) / 256), 256, 0, st>>>(reinterpret_cast<const float4 *>(src),
                                                                 reinterpret_cast<float4 *>(dst), rows, n, d4, 0);

@@ -22,7 +22,7 @@ STATUS_NAMES = ["EMB_OK", "EMB_ERR_INVALID", "EMB_ERR_RANGE", "EMB_ERR_STATE", "
                 "EMB_ERR_NCCL"]
 EMB_MAX_WORLD = 16
 POOL = {"sum": 0, "mean": 1}
-OPT = {"sgd": 0, "adagrad": 1}
+OPT = {"sgd": 0, "adagrad": 1, "rowwise_adagrad": 2}
 SHARD = {"cyclic": 0, "block": 1}
 
 # every symbol include/emb.h declares (checked by tests/test_abi.py)
@@ -209,9 +209,14 @@ class EmbeddingLayer:
     def read_rows(self, table: int, rows) -> Tuple[np.ndarray, np.ndarray]:
         r = np.ascontiguousarray(rows, dtype=np.int64)
         w = np.empty((r.size, self.dim), np.float32)
-        a = np.empty((r.size, self.dim), np.float32)
+        a = np.empty((r.size, self.accum_width), np.float32)
         self._check(lib().emb_read_rows(self.h, table, _ptr(r), r.size, _ptr(w), _ptr(a)), "emb_read_rows")
         return w, a
+
+    @property
+    def accum_width(self) -> int:
+        """Optimizer-state floats per row: 1 for row-wise Adagrad, else D."""
+        return 1 if self.opt == "rowwise_adagrad" else self.dim
 
     def write_rows(self, table: int, rows, w, a=None):
         r = np.ascontiguousarray(rows, dtype=np.int64)

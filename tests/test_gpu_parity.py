@@ -51,7 +51,7 @@ def _read_global(layer, cfg, g):
     """Read fused rows g (all owned by this W=1 layer) -> (w, a)."""
     t = np.searchsorted(cfg.base, g, side="right") - 1
     w = np.empty((g.size, cfg.dim), np.float32)
-    a = np.empty((g.size, cfg.dim), np.float32)
+    a = np.empty((g.size, cfg.accum_width), np.float32)
     for tt in np.unique(t):
         m = t == tt
         w[m], a[m] = layer.read_rows(int(tt), g[m] - cfg.base[tt])
@@ -89,7 +89,7 @@ def _parity_run(torch, wl, B, steps, lr, resync=True, empty_frac=0.0, check_all_
             w, a = _read_global(layer, cfg, rows)
             wo, ao = ora.rows(rows)
             _check_close(w, wo, f"w step {k}")
-            if wl.opt == "adagrad":
+            if wl.opt in ("adagrad", "rowwise_adagrad"):
                 _check_close(a, ao, f"a step {k}")
     finally:
         layer.close()
@@ -114,6 +114,20 @@ def test_dims(torch, dim):
     wl = synthgen.WORKLOADS["C1"].with_(dim=dim, rows=(5000, 3000), slot_table=(0, 1, 1), ids="zipf", zipf_s=1.1,
                                         opt="adagrad", pool="mean")
     _parity_run(torch, wl, 300, steps=2, lr=0.1, empty_frac=0.05)
+
+
+# row-wise Adagrad (reading R14'): compile-time dims, the generic-D path (100), mean
+# pooling and the long hot segments that cross warp ranges (ticket combine)
+@pytest.mark.parametrize("dim,pool", [(16, "sum"), (64, "mean"), (100, "sum"), (128, "sum"), (256, "mean")])
+def test_rowwise_adagrad_dims(torch, dim, pool):
+    wl = synthgen.WORKLOADS["C1"].with_(dim=dim, rows=(5000, 3000), slot_table=(0, 1, 1), ids="zipf", zipf_s=1.1,
+                                        opt="rowwise_adagrad", pool=pool, init_accum=0.1)
+    _parity_run(torch, wl, 300, steps=3, lr=0.1, empty_frac=0.05)
+
+
+def test_rowwise_adagrad_c2_and_hot(torch):
+    _parity_run(torch, synthgen.WORKLOADS["C2"].with_(opt="rowwise_adagrad"), 1024, steps=2, lr=0.01)
+    _parity_run(torch, synthgen.WORKLOADS["C5"].with_(opt="rowwise_adagrad"), 128, steps=2, lr=0.01)
 
 
 def test_c2_reduced_batch_full_tables(torch):
