@@ -89,6 +89,22 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
 __device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void *src_gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src_gmem) : "memory");
 }
+// end-of-kernel hand-off (thread 0 of every block, after the block's work): the last block of the
+// kernel bumps kern_ctr; the last of `nkern` concurrently running kernels copies the sticky device
+// error word to the mapped host word (replaces a separate publish launch after the stream join)
+__device__ __forceinline__ void finish_publish(uint32_t *blk_ctr, uint32_t *kern_ctr, uint32_t nkern,
+                                               uint32_t *err, uint32_t *err_host) {
+  __threadfence();
+  if (atomicAdd(blk_ctr, 1u) != gridDim.x - 1) return;
+  *blk_ctr = 0;
+  __threadfence();
+  if (atomicAdd(kern_ctr, 1u) != nkern - 1) return;
+  *kern_ctr = 0;
+  __threadfence();
+  *(volatile uint32_t *)err_host = atomicOr(err, 0u);
+  __threadfence_system();
+}
+
 __device__ __forceinline__ void cp_async4(uint32_t dst_smem, const void *src_gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst_smem), "l"(src_gmem) : "memory");
 }

@@ -82,7 +82,7 @@ struct emb_ctx {
   double *partials = nullptr;
   uint32_t *tickets = nullptr;
   uint32_t *useg = nullptr, *ukey = nullptr, *ustart = nullptr, *uend = nullptr, *u_count = nullptr,
-           *uniq_status = nullptr, *uniq_counter = nullptr;
+           *uniq_status = nullptr, *uniq_counter = nullptr, *fin = nullptr;
   // world == 1 per-table sort (segsort.cu): table groups of the slot-major CSR
   bool segsort_ok = false;
   int32_t G = 0, segK = 1;
@@ -438,6 +438,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   bad |= dalloc(h, &h->u_count, 2) != cudaSuccess;
   bad |= dalloc(h, &h->uniq_status, unique_status_words(sort_n)) != cudaSuccess;
   bad |= dalloc(h, &h->uniq_counter, 1) != cudaSuccess;
+  bad |= dalloc(h, &h->fin, 3) != cudaSuccess;
   bad |= dalloc(h, &h->err_dev, 1) != cudaSuccess;
   if (W > 1) {
     bad |= dalloc(h, &h->inv, N) != cudaSuccess;
@@ -508,6 +509,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
     }
   }
   CUDA_TRY(h, cudaMemset(h->err_dev, 0, sizeof(uint32_t)));
+  CUDA_TRY(h, cudaMemset(h->fin, 0, 3 * sizeof(uint32_t)));
   CUDA_TRY(h, cudaMemset(h->u_count, 0, 2 * sizeof(uint32_t)));
   void *hp = nullptr;
   if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) != cudaSuccess)
@@ -660,6 +662,8 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
       sa.run_i = h->run_i;
       sa.K = h->segK;
       sa.err = h->err_dev;
+      sa.err_host = h->err_host_dev;
+      sa.fin = (batch > 0 && nnz > 0) ? h->fin : nullptr;  // the later of sort / pool publishes the error word
       h->skey = h->k0;
       h->spay = h->v0;
       static int serial = -1;  // experiment knob: EMB_SERIAL=1 runs the sort before the pool (no overlap)
@@ -676,10 +680,12 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     pa.rows_src = h->w;
     pa.nrows_src = h->rows_local;
     pa.row_idx = nullptr;
+    const bool fused_pub = h->segsort_ok && batch > 0 && nnz > 0;
+    pa.fin = fused_pub ? h->fin : nullptr;
     if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
-    if (batch > 0) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
+    if (batch > 0 && !fused_pub) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
     h->U_l = -1;  // computed on demand
     h->state = 1;
     return EMB_OK;

@@ -141,8 +141,10 @@ struct PoolArgs {
   int64_t nrows_src;       // rows in rows_src (bounds guard)
   const uint32_t *row_idx; // nullptr: row = key (W==1); else row = row_idx[j] (inverse -> unique index)
   float *out;
-  uint32_t *err;           // device error word (copied to err_host by block 0)
-  uint32_t *err_host;      // mapped pinned host word (may be null)
+  uint32_t *err;           // device error word
+  uint32_t *err_host;      // mapped pinned host word
+  uint32_t *fin;           // [3] finish counters (pool blocks, sort blocks, kernels) or nullptr: when set,
+                           // the later of pool / segsort to finish publishes err to err_host
 };
 cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st);
 cudaError_t launch_publish_err(const uint32_t *err, uint32_t *err_host, cudaStream_t st);
@@ -229,6 +231,8 @@ struct SegSortArgs {
   uint32_t *run_k, *run_i;  // [nnz] sorted runs (local key, chunk-relative index)
   int32_t K;                // chunks (CTAs) per group
   uint32_t *err;
+  uint32_t *err_host;       // with fin: see PoolArgs::fin
+  uint32_t *fin;
 };
 cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st);
 cudaError_t launch_local_of_unique(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, uint32_t lmask,

@@ -180,6 +180,10 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
       }
     }
   }
+  if (a.fin) {
+    __syncthreads();
+    if (threadIdx.x == 0) finish_publish(a.fin, a.fin + 2, 2, a.err, a.err_host);
+  }
 }
 
 template <int CPL, int RCH, int MINB>

@@ -6,7 +6,8 @@
 // in fused-key order, so sorting the whole array is the same as sorting each group in place.
 //
 // One kernel, K CTAs per table group (v3; v1 = one CTA per group, issue-bound on 26 of 148 SMs; v2 =
-// chunk sorts + a K-way merge by ranking, search-bound):
+// chunk sorts + a K-way merge by ranking, search-bound; v4 = one 1024-thread CTA per group with
+// per-thread 4-bit digit counters, 98 vs 57 us, dropped):
 //  * CTA (g, b) owns the b-th of K equal ranges of the table's local-id space (bucket(local) =
 //    (local * mul) >> 32, monotone, mul = floor(2^32 K / (rows + 1))). Each warp scans a contiguous
 //    1/16 of the group's keys twice: once to count its items below / inside the range (ballots), then
@@ -52,7 +53,7 @@ __device__ __forceinline__ void group_bounds(const SegSortArgs &a, int g, int64_
   lo = lo < 0 ? 0 : (lo > a.nnz ? a.nnz : lo);
   hi = hi < lo ? lo : (hi > a.nnz ? a.nnz : hi);
 }
-__global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_constant__ SegSortArgs a) {
+__device__ __forceinline__ void segsort_range_body(const SegSortArgs &a) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ uint32_t cnt[SS_WARPS][256];
   __shared__ uint32_t part[SS_THREADS / 32];
@@ -212,123 +213,11 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_const
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// k_segsort_cta (v4, experimental: EMB_SEGSORT=cta; slower than v3 on C2, 98 vs 57 us, the 16-way
-// per-thread cursor select costs ~50 instructions per item): one CTA of 1024 threads per table group. Thread t owns the
-// contiguous run [t*ipt, (t+1)*ipt) of the current order, so processing runs in thread order is
-// stable by construction. LSD radix with 4-bit digits: per pass each thread counts its digits in 8
-// registers of packed 16-bit counters, a warp shuffle scan of the packed counters + a per-warp table
-// give every thread its exclusive start per digit, and the thread scatters its items' ordinals. No
-// ballots and no warp-serial read-modify-write chains (the v1-v3 bottlenecks). Groups up to SEG_CAP
-// items keep keys (u32) and the ordinal ping-pong (u16) in shared memory; larger groups use global
-// scratch (u32 ordinals).
-template <typename OrdT>
-__device__ void cta_radix(const SegSortArgs &a, uint32_t *keys, OrdT *oa, OrdT *ob, uint32_t n, uint32_t bits,
-                          uint32_t (*wtot)[8], uint32_t *wex, uint32_t *dbase) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t ipt = (n + 1023u) / 1024u;
-  const uint32_t i0 = tid * ipt, i1 = min(n, i0 + ipt);
-  const int npass = (int)((bits + 3) / 4);
-  for (int pass = 0; pass < npass; ++pass) {
-    const int shift = 4 * pass;
-    uint32_t c[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) c[r] = 0;
-    for (uint32_t i = i0; i < i1; ++i) {
-      const uint32_t o = pass == 0 ? i : (uint32_t)oa[i];
-      const uint32_t d = (keys[o] >> shift) & 15u;
-      c[d >> 1] += 1u << ((d & 1u) * 16u);
-    }
-    uint32_t ex[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      uint32_t x = c[r];
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
-        if (lane >= off) x += y;
-      }
-      ex[r] = x - c[r];
-      if (lane == 31) wtot[w][r] = x;
-    }
+__global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_constant__ SegSortArgs a) {
+  segsort_range_body(a);  // (its early returns are block-uniform)
+  if (a.fin) {
     __syncthreads();
-    if (tid < 16) {  // per digit: exclusive prefix over warps, and the digit's total
-      const int d = tid;
-      uint32_t run = 0;
-      for (int q = 0; q < 32; ++q) {
-        wex[q * 16 + d] = run;
-        run += (wtot[q][d >> 1] >> ((d & 1) * 16)) & 0xFFFFu;
-      }
-      dbase[d] = run;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t run = 0;
-      for (int d = 0; d < 16; ++d) {
-        const uint32_t t = dbase[d];
-        dbase[d] = run;
-        run += t;
-      }
-    }
-    __syncthreads();
-    uint32_t cur[16];
-#pragma unroll
-    for (int d = 0; d < 16; ++d) cur[d] = dbase[d] + wex[w * 16 + d] + ((ex[d >> 1] >> ((d & 1) * 16)) & 0xFFFFu);
-    for (uint32_t i = i0; i < i1; ++i) {
-      const uint32_t o = pass == 0 ? i : (uint32_t)oa[i];
-      const uint32_t d = (keys[o] >> shift) & 15u;
-      uint32_t dst = 0;
-#pragma unroll
-      for (int q = 0; q < 16; ++q)
-        if (q == (int)d) dst = cur[q]++;
-      if (dst < n) ob[dst] = (OrdT)o;
-      else atomicOr(a.err, EMB_DEVERR_INTERNAL);
-    }
-    __syncthreads();
-    OrdT *t = oa;
-    oa = ob;
-    ob = t;
-  }
-  // oa now holds the sorted ordinals (npass >= 1 always: rows >= 1 => bits >= 1)
-  const int g = blockIdx.x;
-  int64_t glo, ghi;
-  group_bounds(a, g, glo, ghi);
-  const uint32_t base = (uint32_t)a.gbase[g];
-  const uint32_t rows = a.grows[g];
-  for (uint32_t i = tid; i < n; i += 1024u) {
-    const uint32_t o = (uint32_t)oa[i];
-    const uint32_t lk = keys[o];
-    a.skey[glo + i] = (lk >= rows) ? EMB_SENTINEL : base + lk;
-    a.spay[glo + i] = (uint32_t)(glo + o);
-  }
-}
-
-__global__ void __launch_bounds__(1024, 1) k_segsort_cta(const __grid_constant__ SegSortArgs a) {
-  extern __shared__ __align__(16) uint32_t sm[];
-  __shared__ uint32_t wtot[32][8];
-  __shared__ uint32_t wex[32 * 16];
-  __shared__ uint32_t dbase[16];
-  const int tid = threadIdx.x;
-  const int g = blockIdx.x;
-  int64_t glo, ghi;
-  group_bounds(a, g, glo, ghi);
-  const uint32_t n = (uint32_t)(ghi - glo);
-  if (n == 0) return;
-  const uint32_t rows = a.grows[g];
-  const uint32_t bits = a.gbits[g];
-  const bool fits = n <= (uint32_t)SEG_CAP;
-  uint32_t *keys = fits ? sm : a.scratch_k + glo;
-#pragma unroll 4
-  for (uint32_t i = tid; i < n; i += 1024u) {
-    const int64_t id = a.ids[glo + i];
-    keys[i] = (id >= 0 && id < (int64_t)rows) ? (uint32_t)id : rows;  // invalid ids (R4) sort last
-  }
-  __syncthreads();
-  if (fits) {
-    uint16_t *oa = reinterpret_cast<uint16_t *>(sm + SEG_CAP);
-    cta_radix<uint16_t>(a, keys, oa, oa + SEG_CAP, n, bits, wtot, wex, dbase);
-  } else {
-    cta_radix<uint32_t>(a, keys, a.scratch_a + glo, a.scratch_b + glo, n, bits, wtot, wex, dbase);
+    if (threadIdx.x == 0) finish_publish(a.fin + 1, a.fin + 2, 2, a.err, a.err_host);
   }
 }
 
@@ -337,22 +226,13 @@ size_t segsort_smem_bytes() { return (size_t)SEG_CHUNK_CAP * 16 + (size_t)SEG_CA
 cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st) {
   if (groups <= 0 || a.nnz <= 0) return cudaSuccess;
   static bool attr = false;
-  const size_t cta_smem = (size_t)SEG_CAP * 4 + (size_t)SEG_CAP * 2 * 2;  // keys + 2 x u16 ordinals
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_segsort_range, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)segsort_smem_bytes());
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_segsort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem);
-    if (e != cudaSuccess) return e;
     attr = true;
   }
-  static int variant = -1;
-  if (variant < 0) {
-    const char *v = getenv("EMB_SEGSORT");  // experiment knob: "cta" selects the v4 per-thread-counter kernel
-    variant = (v && v[0] == 'c') ? 0 : 1;
-  }
-  if (variant == 1) k_segsort_range<<<groups * a.K, SS_THREADS, segsort_smem_bytes(), st>>>(a);
-  else k_segsort_cta<<<groups, 1024, cta_smem, st>>>(a);
+  k_segsort_range<<<groups * a.K, SS_THREADS, segsort_smem_bytes(), st>>>(a);
   return cudaGetLastError();
 }
 
