@@ -82,7 +82,9 @@ struct emb_ctx {
   double *partials = nullptr;
   uint32_t *tickets = nullptr;
   uint32_t *useg = nullptr, *ukey = nullptr, *ustart = nullptr, *uend = nullptr, *u_count = nullptr,
-           *uniq_status = nullptr, *uniq_counter = nullptr, *fin = nullptr;
+           *uniq_counter = nullptr, *fin = nullptr;
+  uint64_t *uniq_status = nullptr, *ouniq_status = nullptr;
+  uint32_t uniq_epoch = 0, ouniq_epoch = 0;
   // world == 1 per-table sort (segsort.cu): table groups of the slot-major CSR
   bool segsort_ok = false;
   int32_t G = 0, segK = 1;
@@ -106,7 +108,7 @@ struct emb_ctx {
   bool ukey_is_g = false;        // requester unique keys are fused keys g (segsort path) or routing keys
   bool owner_unique_done = false;
   uint32_t *ouseg = nullptr, *oukey = nullptr, *oustart = nullptr, *ouend = nullptr, *ou_count = nullptr,
-           *ouniq_status = nullptr, *ouniq_counter = nullptr;  // owner-side dedup of the received keys
+           *ouniq_counter = nullptr;  // owner-side dedup of the received keys
   int64_t *d_counts = nullptr;       // [2][EMB_MAX_WORLD] send, recv
   int64_t *h_counts = nullptr;       // pinned [2*EMB_MAX_WORLD + 1]
   int64_t recv_cap = 0;
@@ -510,6 +512,12 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   }
   CUDA_TRY(h, cudaMemset(h->err_dev, 0, sizeof(uint32_t)));
   CUDA_TRY(h, cudaMemset(h->fin, 0, 3 * sizeof(uint32_t)));
+  CUDA_TRY(h, cudaMemset(h->uniq_counter, 0, sizeof(uint32_t)));
+  CUDA_TRY(h, cudaMemset(h->uniq_status, 0, sizeof(uint64_t) * unique_status_words(sort_n)));
+  if (h->ouniq_status) {
+    CUDA_TRY(h, cudaMemset(h->ouniq_counter, 0, sizeof(uint32_t)));
+    CUDA_TRY(h, cudaMemset(h->ouniq_status, 0, sizeof(uint64_t) * unique_status_words(h->recv_cap)));
+  }
   CUDA_TRY(h, cudaMemset(h->u_count, 0, 2 * sizeof(uint32_t)));
   void *hp = nullptr;
   if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) != cudaSuccess)
@@ -718,7 +726,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     h->skey = h->k0;
     h->spay = h->v0;
     if (batch > 0) LAUNCH(h, KID_SORT_PASS, st, launch_segsort(sa, h->G, st));
-    UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter};
+    UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter, ++h->uniq_epoch};
     LAUNCH(h, KID_UNIQUE, st, launch_unique(ua, st));
     LAUNCH(h, KID_ROUTE, st,
            launch_partition(h->ukey, h->u_count, nnz, h->ks, h->tcnt, h->send_keys, h->sp, h->d_counts, st));
@@ -729,7 +737,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
                          &h->skey, &h->spay, &nl, prof_hook, h);
     if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
     h->launches += nl;
-    UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter};
+    UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter, ++h->uniq_epoch};
     LAUNCH(h, KID_UNIQUE, st, launch_unique(ua, st));
     LAUNCH(h, KID_ROUTE, st, launch_owner_counts(h->ukey, h->u_count, W, h->ks.lbits, h->d_counts, st));
     LAUNCH(h, KID_ROUTE, st, launch_scatter_inverse(h->skey, h->spay, h->useg, nnz, h->inv, st));
@@ -946,7 +954,7 @@ emb_status_t ensure_unique(emb_ctx *h) {
   if (h->U_l >= 0) return EMB_OK;
   // world == 1: the step itself never needs the compacted unique list; build it on demand
   cudaStream_t st = h->last_stream;
-  UniqueArgs ua{h->skey, h->nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter};
+  UniqueArgs ua{h->skey, h->nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter, ++h->uniq_epoch};
   CUDA_TRY(h, launch_unique(ua, st));
   uint32_t u = 0;
   CUDA_TRY(h, cudaMemcpyAsync(&u, h->u_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -964,7 +972,7 @@ emb_status_t ensure_owner_unique(emb_ctx *h) {
   if (h->world == 1 || h->owner_unique_done || h->n_recv <= 0) return EMB_OK;
   cudaStream_t st = h->last_stream;
   UniqueArgs ua{h->okey, h->n_recv, h->ouseg, h->oukey, h->oustart, h->ouend, h->ou_count, h->ouniq_status,
-                h->ouniq_counter};
+                h->ouniq_counter, ++h->ouniq_epoch};
   CUDA_TRY(h, launch_unique(ua, st));
   CUDA_TRY(h, cudaStreamSynchronize(st));
   h->owner_unique_done = true;

@@ -195,8 +195,10 @@ struct UniqueArgs {
   const uint32_t *skey;
   int64_t n;
   uint32_t *useg, *ukey, *ustart, *uend, *u_count;
-  uint32_t *status;  // [tiles] zeroed
-  uint32_t *counter; // zeroed
+  uint64_t *status;  // [tiles] look-back words tagged with `epoch` (stale words of earlier launches
+                     // read as "not ready": no per-launch memset)
+  uint32_t *counter; // tile ticket; zero before the first launch, reset by the last tile
+  uint32_t epoch;    // distinct per launch on the same status buffer (caller increments, never 0)
 };
 size_t unique_status_words(int64_t max_n);
 cudaError_t launch_unique(const UniqueArgs &a, cudaStream_t st);

@@ -13,7 +13,7 @@ namespace {
 constexpr int UQ_THREADS = 512;
 constexpr int UQ_ITEMS = 8;
 constexpr int UQ_TILE = UQ_THREADS * UQ_ITEMS;
-constexpr uint32_t UF_AGG = 1u << 30, UF_INC = 2u << 30, UF_MASK = (1u << 30) - 1u;
+constexpr uint32_t UF_AGG = 1u << 30, UF_INC = 2u << 30, UF_MASK = (1u << 30) - 1u;  // low word; epoch high
 }  // namespace
 
 size_t unique_status_words(int64_t max_n) { return (size_t)((max_n + UQ_TILE - 1) / UQ_TILE + 1) + 1; }
@@ -22,7 +22,10 @@ __global__ void __launch_bounds__(UQ_THREADS) k_unique(const __grid_constant__ U
   __shared__ uint32_t s_tile, s_excl;
   __shared__ uint32_t warp_tot[UQ_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(a.counter, 1u);
+  if (tid == 0) {
+    s_tile = atomicAdd(a.counter, 1u);
+    if (s_tile == gridDim.x - 1) *a.counter = 0;  // last ticket of this launch: ready for the next one
+  }
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t base = tile * UQ_TILE + (int64_t)tid * UQ_ITEMS;
@@ -49,23 +52,24 @@ __global__ void __launch_bounds__(UQ_THREADS) k_unique(const __grid_constant__ U
     if (lane < UQ_THREADS / 32) warp_tot[lane] = ti - t;  // exclusive warp offsets
     const uint32_t total = __shfl_sync(0xffffffffu, ti, UQ_THREADS / 32 - 1);
     if (lane == 0) {
-      volatile uint32_t *st = a.status + tile;
+      volatile unsigned long long *st = reinterpret_cast<volatile unsigned long long *>(a.status) + tile;
+      const unsigned long long tag = (unsigned long long)a.epoch << 32;
       uint32_t excl = 0;
       if (tile == 0) {
-        *st = UF_INC | total;
+        *st = tag | UF_INC | total;
       } else {
-        *st = UF_AGG | total;
+        *st = tag | UF_AGG | total;
         int64_t look = tile - 1;
         while (true) {
-          uint32_t s;
+          unsigned long long s;
           do {
-            s = *(volatile uint32_t *)(a.status + look);
-          } while ((s & ~UF_MASK) == 0);
-          excl += s & UF_MASK;
-          if (s & UF_INC) break;
+            s = reinterpret_cast<volatile unsigned long long *>(a.status)[look];
+          } while ((s >> 32) != a.epoch || ((uint32_t)s & ~UF_MASK) == 0);
+          excl += (uint32_t)s & UF_MASK;
+          if ((uint32_t)s & UF_INC) break;
           --look;
         }
-        *st = UF_INC | (excl + total);
+        *st = tag | UF_INC | (excl + total);
       }
       s_excl = excl;
       if (tile == (int64_t)gridDim.x - 1) *a.u_count = excl + total;
@@ -89,10 +93,6 @@ __global__ void __launch_bounds__(UQ_THREADS) k_unique(const __grid_constant__ U
 
 cudaError_t launch_unique(const UniqueArgs &a, cudaStream_t st) {
   const int64_t tiles = a.n > 0 ? (a.n + UQ_TILE - 1) / UQ_TILE : 1;
-  cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), st);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(a.status, 0, sizeof(uint32_t) * (size_t)tiles, st);
-  if (e != cudaSuccess) return e;
   k_unique<<<(unsigned)tiles, UQ_THREADS, 0, st>>>(a);
   return cudaGetLastError();
 }
