@@ -623,8 +623,9 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   ka.drow = h->drow;
   ka.blen = h->blen;
   ka.err = h->err_dev;
-  // W == 1 with the per-table sort: pool and sort read the ids themselves (no key kernel)
-  const bool direct = h->world == 1 && h->segsort_ok;
+  // with the per-table sort, the pool and the sort read the ids themselves (no key kernel); at W > 1
+  // the pool then takes each occurrence's received row through row_idx
+  const bool direct = h->segsort_ok;
   if (batch > 0 && !direct) LAUNCH(h, KID_KEYS, st, launch_keys(ka, st));
 
   PoolArgs pa{};
@@ -690,6 +691,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     pa.row_idx = nullptr;
     const bool fused_pub = h->segsort_ok && batch > 0 && nnz > 0;
     pa.fin = fused_pub ? h->fin : nullptr;
+    pa.fin_kernels = 2;
     if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
@@ -760,8 +762,10 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
     h->okey = h->ok0;
     h->opay = h->ov0;
+    const bool fused_pub = batch > 0 && direct;  // the later of merge / pool publishes the error word
     LAUNCH(h, KID_MERGE, h->side,
-           launch_merge_runs(h->recv_keys, h->rt->recv_counts, W, cap, h->okey, h->opay, h->err_dev, h->side));
+           launch_merge_runs(h->recv_keys, h->rt->recv_counts, W, cap, h->okey, h->opay, h->err_dev, h->side,
+                             fused_pub ? h->fin : nullptr, h->err_host_dev));
     // X2 fused with the gather (its last block raises ROWS)
     LAUNCH(h, KID_OWNER_GATHER, st,
            launch_gather_push(px, h->w, h->recv_keys, h->D, cap, h->rows_local, h->err_dev, st));
@@ -769,10 +773,12 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     pa.rows_src = h->uniq_rows;
     pa.nrows_src = h->max_ids;
     pa.row_idx = h->inv;
+    pa.fin = fused_pub ? h->fin : nullptr;
+    pa.fin_kernels = 2;
     if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
-    if (batch > 0) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
+    if (batch > 0 && !fused_pub) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
     h->counts_synced = false;
     h->U_l = -1;
     h->n_recv = -1;

@@ -143,8 +143,10 @@ struct PoolArgs {
   float *out;
   uint32_t *err;           // device error word
   uint32_t *err_host;      // mapped pinned host word
-  uint32_t *fin;           // [3] finish counters (pool blocks, sort blocks, kernels) or nullptr: when set,
-                           // the later of pool / segsort to finish publishes err to err_host
+  uint32_t *fin;           // [3] finish counters (pool blocks, other kernel's blocks, kernels) or nullptr:
+                           // when set, the last of the fin_kernels concurrently running kernels (pool +
+                           // segsort at W = 1, pool + owner merge at W > 1) publishes err to err_host
+  uint32_t fin_kernels;
 };
 cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st);
 cudaError_t launch_publish_err(const uint32_t *err, uint32_t *err_host, cudaStream_t st);
@@ -245,7 +247,8 @@ cudaError_t launch_partition(const uint32_t *ukey, const uint32_t *u_count, int6
 cudaError_t launch_outidx(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, const uint32_t *sp,
                           int64_t n, uint32_t *outidx, uint32_t *inv, cudaStream_t st);
 cudaError_t launch_merge_runs(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t n, uint32_t *okey,
-                              uint32_t *opay, uint32_t *err, cudaStream_t st);
+                              uint32_t *opay, uint32_t *err, cudaStream_t st, uint32_t *fin = nullptr,
+                              uint32_t *err_host = nullptr);
 cudaError_t launch_owner_gather(const float *w, const uint32_t *local, int64_t n, int32_t dim, float *out,
                                 cudaStream_t st);
 

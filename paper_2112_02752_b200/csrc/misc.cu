@@ -29,11 +29,21 @@ __global__ void __launch_bounds__(UQ_THREADS) k_unique(const __grid_constant__ U
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t base = tile * UQ_TILE + (int64_t)tid * UQ_ITEMS;
-  uint32_t k[UQ_ITEMS + 1];
-  uint32_t prev = EMB_SENTINEL;
-  if (base > 0 && base - 1 < a.n) prev = a.skey[base - 1];
+  // the tile's keys (+ one before, one after) staged through shared memory with coalesced loads
+  __shared__ uint32_t s_k[UQ_TILE + 2];
+  const int64_t t0 = tile * UQ_TILE;
 #pragma unroll
-  for (int i = 0; i <= UQ_ITEMS; ++i) k[i] = (base + i < a.n) ? a.skey[base + i] : EMB_SENTINEL;
+  for (int i = 0; i < UQ_ITEMS; ++i) {
+    const int64_t p = t0 + i * UQ_THREADS + tid;
+    s_k[1 + i * UQ_THREADS + tid] = p < a.n ? a.skey[p] : EMB_SENTINEL;
+  }
+  if (tid == 0) s_k[0] = (t0 > 0 && t0 - 1 < a.n) ? a.skey[t0 - 1] : EMB_SENTINEL;
+  if (tid == 1) s_k[UQ_TILE + 1] = (t0 + UQ_TILE < a.n) ? a.skey[t0 + UQ_TILE] : EMB_SENTINEL;
+  __syncthreads();
+  uint32_t k[UQ_ITEMS + 1];
+  const uint32_t prev = s_k[tid * UQ_ITEMS];
+#pragma unroll
+  for (int i = 0; i <= UQ_ITEMS; ++i) k[i] = s_k[1 + tid * UQ_ITEMS + i];
   uint32_t flags = 0, cnt = 0;
 #pragma unroll
   for (int i = 0; i < UQ_ITEMS; ++i) {

@@ -25,8 +25,9 @@ namespace {
 constexpr int POOL_THREADS = 256;
 }  // namespace
 
-// row of occurrence j. Key mode: from the routing key (W > 1: row = inverse[j]). Direct mode (W == 1):
-// g = base[t] + id validated here (R4), and the occurrence's dY row index recorded for the backward.
+// row of occurrence j. Direct mode (per-table sort path): g = base[t] + id validated here (R4), the
+// occurrence's dY row index recorded for the backward, and at W > 1 the row taken from row_idx (the
+// received-row index of the occurrence). Key mode (general sort path): from the routing key.
 __device__ __forceinline__ uint32_t pool_row_of(const PoolArgs &a, int64_t j, uint32_t slot, uint32_t orow) {
   uint32_t row = EMB_SENTINEL;
   if (a.ids) {
@@ -34,6 +35,7 @@ __device__ __forceinline__ uint32_t pool_row_of(const PoolArgs &a, int64_t j, ui
     const int64_t id = a.ids[j];
     if (id >= 0 && id < a.rows[t]) row = (uint32_t)(a.base[t] + (uint64_t)id);
     else atomicOr(a.err, EMB_DEVERR_RANGE);
+    if (row != EMB_SENTINEL && a.row_idx) row = a.row_idx[j];  // W > 1: index of the received row
     a.drow[j] = orow;
   } else {
     const uint32_t k = a.key[j];
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
   }
   if (a.fin) {
     __syncthreads();
-    if (threadIdx.x == 0) finish_publish(a.fin, a.fin + 2, 2, a.err, a.err_host);
+    if (threadIdx.x == 0) finish_publish(a.fin, a.fin + 2, a.fin_kernels, a.err, a.err_host);
   }
 }
 

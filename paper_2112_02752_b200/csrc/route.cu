@@ -54,21 +54,37 @@ __global__ void __launch_bounds__(PT_THREADS) k_part_scatter(const uint32_t *__r
                                                              int64_t *__restrict__ send_counts) {
   __shared__ uint32_t base[EMB_MAX_WORLD];              // global start of (this tile, owner)
   __shared__ uint32_t wcnt[PT_THREADS / 32][EMB_MAX_WORLD];
+  __shared__ uint32_t s_before[EMB_MAX_WORLD], s_total[EMB_MAX_WORLD];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int W = ks.world;
   const uint32_t U = *u_count;
   const int tile = blockIdx.x;
-  if (tid < W) {
-    uint32_t before_owner = 0, before_tile = 0, total = 0;
-    for (int t = 0; t < ntiles; ++t) {
-      const uint32_t v = tcnt[t * EMB_MAX_WORLD + tid];
-      total += v;
-      if (t < tile) before_tile += v;
+  // per owner: totals over all tiles and the part before this tile; warp d sums column d of the
+  // (tile, owner) count matrix with coalesced loads and a warp reduction (not one thread per owner
+  // walking every tile: that serial loop was most of this kernel's time)
+  for (int d = w; d < W; d += PT_THREADS / 32) {
+    uint32_t tot = 0, bef = 0;
+    for (int t = lane; t < ntiles; t += 32) {
+      const uint32_t v = tcnt[t * EMB_MAX_WORLD + d];
+      tot += v;
+      bef += t < tile ? v : 0u;
     }
-    for (int d = 0; d < tid; ++d)
-      for (int t = 0; t < ntiles; ++t) before_owner += tcnt[t * EMB_MAX_WORLD + d];
-    base[tid] = before_owner + before_tile;
-    if (tile == 0) send_counts[tid] = total;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      bef += __shfl_xor_sync(0xffffffffu, bef, o);
+    }
+    if (lane == 0) {
+      s_total[d] = tot;
+      s_before[d] = bef;
+    }
+  }
+  __syncthreads();
+  if (tid < W) {
+    uint32_t before_owner = 0;
+    for (int d = 0; d < tid; ++d) before_owner += s_total[d];
+    base[tid] = before_owner + s_before[tid];
+    if (tile == 0) send_counts[tid] = s_total[tid];
   }
   const uint32_t t0 = tile * PT_TILE;
   // per-warp counts over the warp's contiguous 256 keys
@@ -148,7 +164,7 @@ cudaError_t launch_outidx(const uint32_t *skey, const uint32_t *spay, const uint
 // owner side: stable W-way merge of the received runs (counts in recv_counts[0..W))
 __global__ void k_merge_runs(const uint32_t *__restrict__ rkeys, const int64_t *__restrict__ recv_counts, int W,
                              int64_t cap, uint32_t *__restrict__ okey, uint32_t *__restrict__ opay,
-                             uint32_t *err) {
+                             uint32_t *err, uint32_t *fin, uint32_t *err_host) {
   __shared__ int64_t start[EMB_MAX_WORLD + 1];
   if (threadIdx.x == 0) {
     start[0] = 0;
@@ -181,12 +197,17 @@ __global__ void k_merge_runs(const uint32_t *__restrict__ rkeys, const int64_t *
     okey[pos] = k;
     opay[pos] = (uint32_t)i;
   }
+  if (fin) {  // the later of this merge and the pool publishes the error word (PoolArgs::fin)
+    __syncthreads();
+    if (threadIdx.x == 0) finish_publish(fin + 1, fin + 2, 2, err, err_host);
+  }
 }
 cudaError_t launch_merge_runs(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t n, uint32_t *okey,
-                              uint32_t *opay, uint32_t *err, cudaStream_t st) {
+                              uint32_t *opay, uint32_t *err, cudaStream_t st, uint32_t *fin, uint32_t *err_host) {
   if (n <= 0) return cudaSuccess;
   const int64_t blocks = (n + 255) / 256;
-  k_merge_runs<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(rkeys, recv_counts, W, n, okey, opay, err);
+  k_merge_runs<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(rkeys, recv_counts, W, n, okey, opay, err,
+                                                                          fin, err_host);
   return cudaGetLastError();
 }
 
