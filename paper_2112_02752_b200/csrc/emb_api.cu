@@ -900,11 +900,20 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
     g.useg = h->outidx;
     g.nout = h->max_ids;
     g.p2p = px;
+    static int push = -1;  // experiment knob: EMB_GRAD_PUSH=1 -> local merge (MODE 2) + streaming push
+    if (push < 0) push = getenv("EMB_GRAD_PUSH") ? atoi(getenv("EMB_GRAD_PUSH")) : 0;
+    if (push && g.n > 0) {
+      g.sink_mode = 1;
+      g.out_rows = h->gloc;
+      LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
+      LAUNCH(h, KID_NCCL, st, launch_push_rows(px, h->gloc, h->D, h->max_ids, st));
+    } else {
     g.signal_kind = P2P_GRADS;  // the last warp of the requester grad raises GRADS
     if (g.n > 0)
       LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
     else
       LAUNCH(h, KID_NCCL, st, launch_signal(px, P2P_GRADS, st));
+    }
     // owner: merge the W sources' gradients per row (source-rank order) and apply
     GradArgs o = g;
     o.skey = h->okey;

@@ -78,6 +78,7 @@ struct P2PArgs {
   float *peer_uniq_rows[P2P_MAXW];
   float *peer_grecv[P2P_MAXW];
 };
+cudaError_t launch_push_rows(const P2PArgs &a, const float *rows, int dim, int64_t cap, cudaStream_t st);
 cudaError_t launch_xcounts(const P2PArgs &a, const int64_t *send_counts, uint32_t *err, cudaStream_t st);
 // device helpers (p2p_dev.cuh): the producing kernels (push_keys, gather_push, grad MODE 3) raise
 // their exchange flag from their last block / warp

@@ -136,6 +136,31 @@ __global__ void k_gather_push(P2PArgs a, const float4 *__restrict__ w, const uin
   }
   p2p_signal_last_block(a, P2P_ROWS);
 }
+// X3 as a separate stream (experiment knob EMB_GRAD_PUSH=1): the requester's merged gradient rows,
+// written locally in send order (grad MODE 2), streamed to each owner's receive buffer with
+// contiguous float4 stores; the last block raises GRADS
+__global__ void k_push_rows(P2PArgs a, const float4 *__restrict__ rows, int d4) {
+  const RouteTable *rt = a.rt;
+  const int W = a.world;
+  const int64_t n = rt->n_send * d4;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = t / d4;
+    const int c = (int)(t - q * d4);
+    const int d = seg_of(rt->soff, W, q);
+    float4 *dst = reinterpret_cast<float4 *>(a.peer_grecv[d]) + (size_t)(rt->dst_off[d] + (q - rt->soff[d])) * d4 + c;
+    *dst = rows[t];
+  }
+  p2p_signal_last_block(a, P2P_GRADS);
+}
+cudaError_t launch_push_rows(const P2PArgs &a, const float *rows, int dim, int64_t cap, cudaStream_t st) {
+  const int d4 = dim / 4;
+  int64_t blocks = (cap * d4 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_push_rows<<<(unsigned)blocks, 256, 0, st>>>(a, reinterpret_cast<const float4 *>(rows), d4);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t *recv_keys, int dim, int64_t cap,
                                int64_t rows_local, uint32_t *err, cudaStream_t st) {
   const int d4 = dim / 4;
