@@ -33,17 +33,17 @@ def main():
     nid = D.share_unique_id(E.get_unique_id)
     case = os.environ.get("EMB_MGPU_CASE", "c3")
     shard = os.environ.get("EMB_MGPU_SHARD", "cyclic")
-    if case in ("c3", "c3rw"):
+    if case in ("c3", "c3rw", "c3full"):
         wl = synthgen.WORKLOADS["C3"]
         if case == "c3rw":  # row-wise Adagrad
             wl = wl.with_(opt="rowwise_adagrad", init_accum=0.1)
-        B = 2048
+        B = wl.batch - 16 * (world - 1) if case == "c3full" else 2048  # c3full: BJ:9 per-GPU batch
     else:  # hot ids, mean pooling, sgd
         wl = synthgen.WORKLOADS["C5"].with_(bag_len=8, pool="mean", opt="sgd")
         B = 256
     cfgW = O.config_from_workload(wl, world=world, shard=shard)
     cfg1 = O.config_from_workload(wl, world=1)
-    steps = 3
+    steps = 2 if case == "c3full" else 3
     bts = [[synthgen.make_batch(wl, rank=r, step=s, batch=B + 16 * r) for r in range(world)] for s in range(steps)]
     layer = make_layer(wl, max_batch=B + 16 * world, max_ids=max(b.nnz for st in bts for b in st), world=world,
                        rank=rank, nccl_id=nid, device=local, shard=shard)

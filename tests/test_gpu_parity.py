@@ -130,6 +130,14 @@ def test_rowwise_adagrad_c2_and_hot(torch):
     _parity_run(torch, synthgen.WORKLOADS["C5"].with_(opt="rowwise_adagrad"), 128, steps=2, lr=0.01)
 
 
+def test_c2_full_size(torch):
+    """C2 at BASELINE's full size (BJ:8: 26 x 10M rows, D=64, B=16,384, Zipf 1.05, Adagrad) through the
+    same device-buffer C-ABI calls bench.py times: every output Y and every touched row of two
+    resynced steps against the oracle (the oracle handles this size in seconds)."""
+    wl = synthgen.WORKLOADS["C2"]
+    _parity_run(torch, wl, wl.batch, steps=2, lr=wl.lr)
+
+
 def test_c2_reduced_batch_full_tables(torch):
     """C2 tables (26 x 10M, D=64, Zipf 1.05, Adagrad) with a reduced batch: 3 resynced steps."""
     wl = synthgen.WORKLOADS["C2"]

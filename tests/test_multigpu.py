@@ -28,7 +28,8 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("case,shard", [("c3", "cyclic"), ("hot", "cyclic"), ("c3", "block"), ("c3rw", "cyclic")])
+@pytest.mark.parametrize("case,shard", [("c3", "cyclic"), ("hot", "cyclic"), ("c3", "block"), ("c3rw", "cyclic"),
+                                            ("c3full", "cyclic")])
 def test_two_gpu_row_sharded_parity(case, shard):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
