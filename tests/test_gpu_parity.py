@@ -138,6 +138,14 @@ def test_c2_full_size(torch):
     _parity_run(torch, wl, wl.batch, steps=2, lr=wl.lr)
 
 
+def test_c4_like_large_keyspace(torch):
+    """C4's structure (BJ:10, R19: 26 slots sharing ONE table, Zipf 1.2) on a 3e8-row table (29-bit
+    keys: four radix passes in the per-table sort), D=32 and SGD so the shard fits one GPU; the full
+    1e9-row x D=128 C4 needs 4-8 GPUs."""
+    wl = synthgen.WORKLOADS["C4"].with_(rows=(300_000_000,), dim=32, opt="sgd")
+    _parity_run(torch, wl, 2048, steps=2, lr=0.05)
+
+
 def test_c2_reduced_batch_full_tables(torch):
     """C2 tables (26 x 10M, D=64, Zipf 1.05, Adagrad) with a reduced batch: 3 resynced steps."""
     wl = synthgen.WORKLOADS["C2"]
