@@ -764,8 +764,8 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     h->opay = h->ov0;
     const bool fused_pub = batch > 0 && direct;  // the later of merge / pool publishes the error word
     LAUNCH(h, KID_MERGE, h->side,
-           launch_merge_runs(h->recv_keys, h->rt->recv_counts, W, cap, h->okey, h->opay, h->err_dev, h->side,
-                             fused_pub ? h->fin : nullptr, h->err_host_dev));
+           launch_merge_tree(h->recv_keys, h->rt->recv_counts, W, cap, h->ok0, h->ov0, h->ok1, h->ov1, h->err_dev,
+                             h->side, fused_pub ? h->fin : nullptr, h->err_host_dev));
     // X2 fused with the gather (its last block raises ROWS)
     LAUNCH(h, KID_OWNER_GATHER, st,
            launch_gather_push(px, h->w, h->recv_keys, h->D, cap, h->rows_local, h->err_dev, st));

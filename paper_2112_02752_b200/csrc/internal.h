@@ -247,6 +247,9 @@ cudaError_t launch_partition(const uint32_t *ukey, const uint32_t *u_count, int6
                              cudaStream_t st);
 cudaError_t launch_outidx(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, const uint32_t *sp,
                           int64_t n, uint32_t *outidx, uint32_t *inv, cudaStream_t st);
+cudaError_t launch_merge_tree(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t cap, uint32_t *ok0,
+                              uint32_t *op0, uint32_t *ok1, uint32_t *op1, uint32_t *err, cudaStream_t st,
+                              uint32_t *fin, uint32_t *err_host);
 cudaError_t launch_merge_runs(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t n, uint32_t *okey,
                               uint32_t *opay, uint32_t *err, cudaStream_t st, uint32_t *fin = nullptr,
                               uint32_t *err_host = nullptr);

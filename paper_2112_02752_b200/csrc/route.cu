@@ -7,10 +7,12 @@
 //    position of every distinct key, and the per-owner counts (X0 payload).
 //  * k_outidx: per sorted occurrence: send position of its key (the row it gets back, and the slot of
 //    its merged gradient in the X3 send buffer); inverse[occurrence] for the pool.
-//  * k_merge_runs: the owner receives W runs (one per source rank), each sorted by local id; a stable
-//    W-way merge by ranking (ties keep source-rank order) replaces a full radix sort of the received
-//    keys: item i of run r goes to (i - start_r) + sum_{r'<r} upper_bound(r', k) + sum_{r'>r}
-//    lower_bound(r', k).
+//  * k_merge_pass: the owner receives W runs (one per source rank), each sorted by local id; a stable
+//    merge tree (ceil(log2 W) passes of pairwise merge-path merges, ties keep the lower source rank)
+//    replaces a full radix sort of the received keys. Per pass, a CTA owns TILE outputs of one merged
+//    run: one merge-path search for its two diagonals, the A / B windows staged in shared memory, then
+//    per-thread searches and sequential merges there. (v1, k_merge_runs: every item ranked by binary
+//    searches into the W-1 other runs — 60 / 106 us at W = 2 / 4, growing with W.)
 #include "../../include/emb.h"
 #include "common.cuh"
 #include "internal.h"
@@ -161,7 +163,130 @@ cudaError_t launch_outidx(const uint32_t *skey, const uint32_t *spay, const uint
   return cudaGetLastError();
 }
 
-// owner side: stable W-way merge of the received runs (counts in recv_counts[0..W))
+// ---- merge tree (v2)
+namespace {
+constexpr int MP_THREADS = 256;
+constexpr int MP_ITEMS = 8;
+constexpr int MP_TILE = MP_THREADS * MP_ITEMS;  // outputs per CTA
+}  // namespace
+
+// number of A items among the first d outputs of the stable merge of A (first) and B
+__device__ __forceinline__ int64_t merge_path(const uint32_t *A, int64_t m, const uint32_t *B, int64_t n, int64_t d) {
+  int64_t lo = d > n ? d - n : 0, hi = d < m ? d : m;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (A[mid] <= B[d - 1 - mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// pass r: output run j = stable merge of sources [2j*w, (2j+1)*w) (A) and [(2j+1)*w, (2j+2)*w) (B),
+// w = 2^r. ip == nullptr: payload = receive position (first pass).
+__global__ void __launch_bounds__(MP_THREADS) k_merge_pass(const uint32_t *__restrict__ ik,
+                                                           const uint32_t *__restrict__ ip,
+                                                           const int64_t *__restrict__ recv_counts, int W, int w,
+                                                           uint32_t *__restrict__ ok, uint32_t *__restrict__ op,
+                                                           uint32_t *err, uint32_t *fin, uint32_t *err_host) {
+  __shared__ int64_t P[EMB_MAX_WORLD + 1];
+  __shared__ uint32_t sk[MP_TILE], sp[MP_TILE];
+  __shared__ int64_t s_a0, s_am, s_b0, s_bn, s_i0, s_i1, s_d0, s_d1, s_out;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    P[0] = 0;
+    for (int r = 0; r < W; ++r) P[r + 1] = P[r] + recv_counts[r];
+  }
+  __syncthreads();
+  const int nruns = (W + 2 * w - 1) / (2 * w);
+  // block -> (output run j, tile within the run)
+  int j = -1;
+  int64_t tile = blockIdx.x;
+  for (int q = 0; q < nruns; ++q) {
+    const int64_t len = P[min(W, (2 * q + 2) * w)] - P[min(W, 2 * q * w)];
+    const int64_t nt = (len + MP_TILE - 1) / MP_TILE;
+    if (tile < nt) {
+      j = q;
+      break;
+    }
+    tile -= nt;
+  }
+  if (j >= 0) {
+    if (tid == 0) {
+      const int64_t a0 = P[min(W, 2 * j * w)], b0 = P[min(W, (2 * j + 1) * w)], e = P[min(W, (2 * j + 2) * w)];
+      const int64_t m = b0 - a0, n = e - b0;
+      const int64_t d0 = tile * MP_TILE, d1 = min(d0 + MP_TILE, m + n);
+      s_a0 = a0;
+      s_am = m;
+      s_b0 = b0;
+      s_bn = n;
+      s_d0 = d0;
+      s_d1 = d1;
+      s_i0 = merge_path(ik + a0, m, ik + b0, n, d0);
+      s_i1 = merge_path(ik + a0, m, ik + b0, n, d1);
+      s_out = a0 + d0;  // merged run j starts where its A run started
+    }
+    __syncthreads();
+    const int64_t a0 = s_a0, b0 = s_b0, i0 = s_i0, i1 = s_i1, d0 = s_d0, d1 = s_d1;
+    const int na = (int)(i1 - i0), nb = (int)((d1 - i1) - (d0 - i0));
+    const int64_t bj0 = b0 + (d0 - i0);
+    for (int q = tid; q < na; q += MP_THREADS) {
+      sk[q] = ik[a0 + i0 + q];
+      sp[q] = ip ? ip[a0 + i0 + q] : (uint32_t)(a0 + i0 + q);
+    }
+    for (int q = tid; q < nb; q += MP_THREADS) {
+      sk[na + q] = ik[bj0 + q];
+      sp[na + q] = ip ? ip[bj0 + q] : (uint32_t)(bj0 + q);
+    }
+    __syncthreads();
+    // per thread: MP_ITEMS consecutive outputs of the tile
+    const int dd = tid * MP_ITEMS;
+    const int tot = na + nb;
+    if (dd < tot) {
+      int lo = dd > nb ? dd - nb : 0, hi = dd < na ? dd : na;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sk[mid] <= sk[na + dd - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+      }
+      int ia = lo, ib = dd - lo;
+      const int64_t o = s_out + dd;
+      for (int q = 0; q < MP_ITEMS && dd + q < tot; ++q) {
+        const bool takeA = ib >= nb || (ia < na && sk[ia] <= sk[na + ib]);
+        const int src = takeA ? ia : na + ib;
+        ok[o + q] = sk[src];
+        op[o + q] = sp[src];
+        if (takeA) ++ia;
+        else ++ib;
+      }
+    }
+  }
+  if (fin) {  // last pass: the later of this merge and the pool publishes the error word
+    __syncthreads();
+    if (tid == 0) finish_publish(fin + 1, fin + 2, 2, err, err_host);
+  }
+}
+
+cudaError_t launch_merge_tree(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t cap, uint32_t *ok0,
+                              uint32_t *op0, uint32_t *ok1, uint32_t *op1, uint32_t *err, cudaStream_t st,
+                              uint32_t *fin, uint32_t *err_host) {
+  int passes = 0;
+  while ((1 << passes) < W) ++passes;
+  const int64_t blocks = (cap + MP_TILE - 1) / MP_TILE + W;  // >= sum over runs of their tiles
+  const uint32_t *ik = rkeys, *ip = nullptr;
+  for (int r = 0; r < passes; ++r) {
+    const bool to0 = ((passes - 1 - r) & 1) == 0;  // the last pass lands in (ok0, op0)
+    uint32_t *ok = to0 ? ok0 : ok1, *op = to0 ? op0 : op1;
+    k_merge_pass<<<(unsigned)blocks, MP_THREADS, 0, st>>>(ik, ip, recv_counts, W, 1 << r, ok, op, err,
+                                                          r == passes - 1 ? fin : nullptr, err_host);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ik = ok;
+    ip = op;
+  }
+  return cudaSuccess;
+}
+
+// owner side (v1, kept for the NCCL exchange path): stable W-way merge by ranking
 __global__ void k_merge_runs(const uint32_t *__restrict__ rkeys, const int64_t *__restrict__ recv_counts, int W,
                              int64_t cap, uint32_t *__restrict__ okey, uint32_t *__restrict__ opay,
                              uint32_t *err, uint32_t *fin, uint32_t *err_host) {
