@@ -83,9 +83,18 @@ def state_bytes(wl, U):
     return 8 * D * U
 
 
-def kernel_bytes(name, wl, N, SB, U, W):
-    """Algorithmic bytes of one launch of the named kernel."""
+def kernel_bytes(name, wl, N, SB, U, W, U_l=None):
+    """Algorithmic bytes of one launch of the named kernel. U = distinct rows updated by
+    this GPU (U_o), U_l = distinct keys this GPU requested."""
     D = wl.dim
+    U_l = U if U_l is None else U_l
+    if name == "grad_local":
+        # W > 1 requester merge: dY row + sorted key/payload/dY-row index per occurrence, one merged fp32
+        # row per requested key written (to its owner, (W-1)/W of them over NVLink)
+        return 4 * D * N + 12 * N + 4 * D * U_l
+    if name == "owner_gather":
+        # received key + table row read + row written to the requester, per received key (~U_l per rank)
+        return 4 * U_l + 8 * D * U_l
     if name == "grad_apply":
         # dY row per occurrence + sorted key/payload/bag index per occurrence + state RMW per touched row
         return 4 * D * N + 12 * N + state_bytes(wl, U)
@@ -325,7 +334,7 @@ def main():
 
     # dominant kernel = largest summed device time
     dom, (dom_ms, dom_cnt) = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 0))
-    kb = kernel_bytes(dom, wl, N_mean, SB, U_o, n)
+    kb = kernel_bytes(dom, wl, N_mean, SB, U_o, n, U_l)
     roof = None
     if kb is not None and dom_cnt:
         t_launch = dom_ms / dom_cnt / 1e3
