@@ -38,6 +38,10 @@ def main():
         if case == "c3rw":  # row-wise Adagrad
             wl = wl.with_(opt="rowwise_adagrad", init_accum=0.1)
         B = wl.batch - 16 * (world - 1) if case == "c3full" else 2048  # c3full: BJ:9 per-GPU batch
+    elif case == "gen":  # non-monotone slot -> table map: key kernel + general radix sort + NCCL exchange
+        wl = synthgen.WORKLOADS["C1"].with_(rows=(50_000, 30_000), slot_table=(1, 0, 1), ids="zipf", zipf_s=1.1,
+                                            opt="adagrad", pool="mean")
+        B = 512
     else:  # hot ids, mean pooling, sgd
         wl = synthgen.WORKLOADS["C5"].with_(bag_len=8, pool="mean", opt="sgd")
         B = 256

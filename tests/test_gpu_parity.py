@@ -146,6 +146,15 @@ def test_c4_like_large_keyspace(torch):
     _parity_run(torch, wl, 2048, steps=2, lr=0.05)
 
 
+@pytest.mark.parametrize("opt", ["sgd", "adagrad", "rowwise_adagrad"])
+def test_general_sort_path(torch, opt):
+    """A non-monotone slot -> table map (slot 0 -> table 1, slot 1 -> table 0) cannot use the per-table
+    sort: the key kernel + the general LSD radix sort + the key-mode pool run instead."""
+    wl = synthgen.WORKLOADS["C1"].with_(rows=(50_000, 30_000), slot_table=(1, 0, 1), ids="zipf", zipf_s=1.1,
+                                        opt=opt, pool="mean")
+    _parity_run(torch, wl, 700, steps=3, lr=0.05, empty_frac=0.05)
+
+
 def test_c2_reduced_batch_full_tables(torch):
     """C2 tables (26 x 10M, D=64, Zipf 1.05, Adagrad) with a reduced batch: 3 resynced steps."""
     wl = synthgen.WORKLOADS["C2"]
