@@ -502,12 +502,15 @@ static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
   if (wpc > 8) wpc = 8;
   if (wpc < 1) wpc = 1;
   const size_t smem = per_warp * wpc;
-  static size_t attr = 0;
-  if (attr < smem) {
+  static size_t attr[EMB_MAX_DEVICES] = {};  // per device: the attribute is a per-context setting
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= EMB_MAX_DEVICES) return cudaErrorInvalidDevice;
+  if (attr[dev] < smem) {
     cudaError_t e =
         cudaFuncSetAttribute(k_grad<CPL, T, NS, MEAN, MODE, DC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[dev] = smem;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grad<CPL, T, NS, MEAN, MODE, DC, MINB>, wpc * 32, smem);

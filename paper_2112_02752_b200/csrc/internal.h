@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+constexpr int EMB_MAX_DEVICES = 64;  // per-device launch-attribute caches
+
 namespace emb {
 
 // Sharding / key-space parameters (R7). The ROUTING KEY of a fused row g is

@@ -225,12 +225,15 @@ size_t segsort_smem_bytes() { return (size_t)SEG_CHUNK_CAP * 16 + (size_t)SEG_CA
 
 cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st) {
   if (groups <= 0 || a.nnz <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[EMB_MAX_DEVICES] = {};  // per device: the attribute is a per-context setting
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= EMB_MAX_DEVICES) return cudaErrorInvalidDevice;
+  if (!attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_segsort_range, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)segsort_smem_bytes());
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[dev] = true;
   }
   k_segsort_range<<<groups * a.K, SS_THREADS, segsort_smem_bytes(), st>>>(a);
   return cudaGetLastError();
