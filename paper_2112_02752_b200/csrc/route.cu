@@ -136,8 +136,9 @@ __global__ void __launch_bounds__(PT_THREADS) k_part_scatter(const uint32_t *__r
 cudaError_t launch_partition(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, const KeySpace &ks,
                              uint32_t *tcnt, uint32_t *send_keys, uint32_t *sp, int64_t *send_counts,
                              cudaStream_t st) {
-  const int ntiles = (int)((cap + PT_TILE - 1) / PT_TILE);
-  if (ntiles <= 0) return cudaSuccess;
+  // at least one tile: with no ids this step the per-owner send counts must still be written (zeros),
+  // or the exchange would announce the previous step's counts
+  const int ntiles = cap > 0 ? (int)((cap + PT_TILE - 1) / PT_TILE) : 1;
   k_part_count<<<ntiles, PT_THREADS, 0, st>>>(ukey, u_count, ks, tcnt);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

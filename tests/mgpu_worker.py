@@ -38,6 +38,9 @@ def main():
         if case == "c3rw":  # row-wise Adagrad
             wl = wl.with_(opt="rowwise_adagrad", init_accum=0.1)
         B = wl.batch - 16 * (world - 1) if case == "c3full" else 2048  # c3full: BJ:9 per-GPU batch
+    elif case == "edge":  # ranks with no ids: batch 0 (rank 1, step 1), all bags empty (rank 0, step 2)
+        wl = synthgen.WORKLOADS["C3"].with_(rows=(40_000, 30_000, 20_000), slot_table=(0, 1, 2), pool="mean")
+        B = 512
     elif case == "gen":  # non-monotone slot -> table map: key kernel + general radix sort + NCCL exchange
         wl = synthgen.WORKLOADS["C1"].with_(rows=(50_000, 30_000), slot_table=(1, 0, 1), ids="zipf", zipf_s=1.1,
                                             opt="adagrad", pool="mean")
@@ -48,7 +51,14 @@ def main():
     cfgW = O.config_from_workload(wl, world=world, shard=shard)
     cfg1 = O.config_from_workload(wl, world=1)
     steps = 2 if case == "c3full" else 3
-    bts = [[synthgen.make_batch(wl, rank=r, step=s, batch=B + 16 * r) for r in range(world)] for s in range(steps)]
+    def _batch(r, s_):
+        if case == "edge" and s_ == 1 and r == 1:
+            return synthgen.make_batch(wl, rank=r, step=s_, batch=0)
+        if case == "edge" and s_ == 2 and r == 0:
+            return synthgen.make_batch(wl, rank=r, step=s_, batch=B, empty_frac=1.0)
+        return synthgen.make_batch(wl, rank=r, step=s_, batch=B + 16 * r)
+
+    bts = [[_batch(r, s) for r in range(world)] for s in range(steps)]
     layer = make_layer(wl, max_batch=B + 16 * world, max_ids=max(b.nnz for st in bts for b in st), world=world,
                        rank=rank, nccl_id=nid, device=local, shard=shard)
     ora = O.OracleEmbedding(cfg1)

@@ -31,7 +31,8 @@ def _port():
 @pytest.mark.parametrize("case,shard,exchange", [("c3", "cyclic", "p2p"), ("hot", "cyclic", "p2p"),
                                                  ("c3", "block", "p2p"), ("c3rw", "cyclic", "p2p"),
                                                  ("c3full", "cyclic", "p2p"), ("c3", "cyclic", "nccl"),
-                                                 ("gen", "cyclic", "p2p"), ("hot", "block", "nccl")])
+                                                 ("gen", "cyclic", "p2p"), ("hot", "block", "nccl"),
+                                                 ("edge", "cyclic", "p2p"), ("edge", "block", "nccl")])
 def test_two_gpu_row_sharded_parity(case, shard, exchange):
     """exchange: "p2p" = the peer-memory exchange kernels (default); "nccl" = the v1 grouped
     send/recv exchange (EMB_EXCHANGE=nccl). Case "gen" has a non-monotone slot -> table map, which
