@@ -171,13 +171,18 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
       VecF<CPL> v[RCH];
 #pragma unroll
       for (int r = 0; r < RCH; ++r) {
+        // unconditional loads (a missing row reads row 0 and is zeroed at the store): predicated or
+        // branched loads need one predicate register each, and with only 7 of them ptxas issued the
+        // rows in groups of ~4 between stores instead of RCH in flight
         const uint32_t ri = __shfl_sync(0xffffffffu, row, c0 + r);
-        if (ri != EMB_SENTINEL && active) v[r].load_nc(a.rows_src + (size_t)ri * D + col);
-        else v[r].zero();
+        const bool ok = ri != EMB_SENTINEL && active;
+        v[r].load_nc(a.rows_src + (size_t)(ok ? ri : 0u) * D + (active ? col : 0));
       }
 #pragma unroll
       for (int r = 0; r < RCH; ++r) {
+        const uint32_t ri = __shfl_sync(0xffffffffu, row, c0 + r);
         const uint32_t oi = __shfl_sync(0xffffffffu, orow, c0 + r);
+        if (ri == EMB_SENTINEL) v[r].zero();
         if (c0 + r < nbt && active) v[r].store_cs(a.out + (size_t)oi * D + col);
       }
     }
@@ -217,6 +222,7 @@ cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st) {
   }
   if (a.dim <= 64) {
     if (var == 1) return launch_pool_t<2, 32, 2>(a, ntiles, st);
+    if (var == 7) return launch_pool_t<2, 16, 2>(a, ntiles, st);
     if (var == 2) return launch_pool_t<2, 32, 3>(a, ntiles, st);
     if (var == 3) return launch_pool_t<2, 8, 4>(a, ntiles, st);
     return launch_pool_t<2, 16, 3>(a, ntiles, st);

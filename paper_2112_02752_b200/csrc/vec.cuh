@@ -24,6 +24,25 @@ struct VecF {
       }
     }
   }
+  // read-only streaming load if `pred`, else zeros: a single predicated instruction per 16 / 8 bytes
+  __device__ __forceinline__ void load_nc_pred(const float *p, bool pred) {
+    const uint32_t q = pred;
+    if constexpr (CPL == 2) {
+      asm volatile(
+          "{\n .reg .pred pp;\n setp.ne.u32 pp, %3, 0;\n mov.b32 %0, 0;\n mov.b32 %1, 0;\n"
+          " @pp ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];\n}"
+          : "=f"(v[0]), "=f"(v[1])
+          : "l"(p), "r"(q));
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; c += 4)
+        asm volatile(
+            "{\n .reg .pred pp;\n setp.ne.u32 pp, %5, 0;\n mov.b32 %0, 0;\n mov.b32 %1, 0;\n mov.b32 %2, 0;\n"
+            " mov.b32 %3, 0;\n @pp ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];\n}"
+            : "=f"(v[c]), "=f"(v[c + 1]), "=f"(v[c + 2]), "=f"(v[c + 3])
+            : "l"(p + c), "r"(q));
+    }
+  }
   // coherent load (rows that this kernel also writes: table / optimizer state)
   __device__ __forceinline__ void load(const float *p) {
     if constexpr (CPL == 2) {
