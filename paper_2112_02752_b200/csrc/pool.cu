@@ -103,15 +103,16 @@ __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, in
     nrow = occ_row(jn + lane);  // prefetch
     VecF<CPL> v[RCH];
 #pragma unroll
-    for (int r = 0; r < RCH; ++r) {
+    for (int r = 0; r < RCH; ++r) {  // unconditional loads (see the single-id path in k_pool)
       const uint32_t ri = __shfl_sync(0xffffffffu, row, r);
-      if (ri != EMB_SENTINEL && active) v[r].load_nc(a.rows_src + (size_t)ri * D + col);
-      else v[r].zero();
+      const bool ok = ri != EMB_SENTINEL && active;
+      v[r].load_nc(a.rows_src + (size_t)(ok ? ri : 0u) * D + (active ? col : 0));
     }
 #pragma unroll
     for (int r = 0; r < RCH; ++r) {
       const int64_t j = j0 + r;
       if (j >= hi) break;
+      if (__shfl_sync(0xffffffffu, row, r) == EMB_SENTINEL) v[r].zero();
 #pragma unroll
       for (int c = 0; c < CPL; ++c) acc[c] += (double)v[r].v[c];
       if (j + 1 == cend) {
