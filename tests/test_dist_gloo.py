@@ -1,7 +1,7 @@
-"""World-size-2 CPU tests (gloo) of the N>1 host logic (-m "not gpu"):
+"""World-size-2 and -8 CPU tests (gloo) of the N>1 host logic (-m "not gpu"):
   * the ncclUniqueId broadcast and the max-over-ranks timing reduction of paper_2112_02752_b200.dist;
-  * the row-sharded exchange protocol that libemb implements over NCCL, replayed with
-    torch.distributed all-to-alls and oracle arithmetic per rank: per-rank dedup -> owner-major send
+  * the row-sharded exchange protocol that libemb implements with its peer-memory kernels (or NCCL,
+    DESIGN.md §8), replayed with torch.distributed all-to-alls and oracle arithmetic per rank: per-rank dedup -> owner-major send
     lists + counts (X0) -> keys to owners (X1) -> rows back (X2) -> pool -> per-unique-key gradients
     to owners (X3) -> source-rank-order merge -> update. Its result must equal the single-process
     oracle on the same per-rank batches (SPEC idea "distributed == serial").
@@ -17,9 +17,6 @@ import torch.multiprocessing as mp
 
 import synthgen
 from oracle import emb_oracle as O
-
-W = 2
-
 
 def _free_port():
     s = socket.socket()
@@ -46,7 +43,7 @@ def _a2av(send_chunks):
     return res
 
 
-def _worker(rank, port, q):
+def _worker(rank, W, port, q):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=W)
@@ -113,15 +110,16 @@ def _worker(rank, port, q):
         q.put((rank, False, traceback.format_exc()))
 
 
-@pytest.mark.timeout(300)
-def test_two_rank_exchange_protocol_equals_serial():
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("W", [2, 8])
+def test_exchange_protocol_equals_serial(W):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(W)]
+    ps = [ctx.Process(target=_worker, args=(r, W, port, q)) for r in range(W)]
     for p in ps:
         p.start()
-    res = [q.get(timeout=280) for _ in range(W)]
+    res = [q.get(timeout=560) for _ in range(W)]
     for p in ps:
         p.join(timeout=60)
     for rank, ok, err in res:
