@@ -7,7 +7,8 @@ update) through the C-ABI library, on synthetic BASELINE.json workloads.
 N = 1 : workload C2 (BJ:8, the config BASELINE's metric is quoted on): 26 slots x 10M rows/table,
         D = 64, B = 16,384, Zipf(1.05) ids, element-wise Adagrad, sum pooling.
 N > 1 : workload C3 (BJ:9) row-sharded (cyclic) over N GPUs, B = 16,384 per GPU (weak scaling),
-        launched with torchrun (one process per GPU, NCCL all-to-alls inside libemb).
+        launched with torchrun (one process per GPU; libemb exchanges ids / rows / gradients over
+        NVLink peer memory with its own kernels).
 --impl reference: the CPU oracle (oracle/, NumPy fp64) timed on the host cores on a bounded sample of
         the same workload (rank 0 only).
 

@@ -110,20 +110,21 @@ emb_status_t emb_destroy(emb_handle_t h);
 /* Write a fresh 128-byte ncclUniqueId to out128 (host). Call on rank 0 and broadcast. */
 emb_status_t emb_get_unique_id(void *out128);
 
-/* ---- the step (enqueued on cuda_stream; no host sync when world == 1) ------------------------ */
+/* ---- the step (enqueued on cuda_stream; no host synchronisation) ---------------------------- */
 
 /* Forward: out[b][s][:] = sum (or mean) over bag (s,b) of W_t[id][:]  (R1-R5).
  * ids: device int64 [nnz]; offsets: device int64 [S*batch+1]; out: device fp32 [batch][S][D],
  * 16-byte aligned. 0 <= batch <= max_batch, 0 <= nnz <= max_ids. Also dedups the ids per rank and,
- * when world > 1, routes the unique keys to their owners and returns the rows over NCCL (collective;
- * the host waits for the per-peer key counts). Saves what backward needs in the workspace, so ids
- * and offsets may be reused once the stream work completes. */
+ * when world > 1, routes the unique keys to their owners and returns the rows (collective: device-side
+ * exchange over NVLink peer memory, or NCCL grouped send/recv with one host wait for the per-peer
+ * counts when EMB_EXCHANGE=nccl or the slot -> table map is not monotone). Saves what backward needs
+ * in the workspace, so ids and offsets may be reused once the stream work completes. */
 emb_status_t emb_lookup(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                         int64_t nnz, float *out, void *cuda_stream);
 
 /* Backward + update for the last lookup: c_j = d_out[b][s][:] (mean: / |bag|), G[g] = sum of c_j over
  * all occurrences of all ranks (fp64 accumulation, deterministic order), then one SGD or element-wise
- * Adagrad update per touched row (R8-R14). d_out: device fp32 [batch][S][D], 16-byte aligned.
+ * Adagrad (or row-wise Adagrad) update per touched row (R8-R14'). d_out: device fp32 [batch][S][D], 16-byte aligned.
  * Collective when world > 1. */
 emb_status_t emb_backward_update(emb_handle_t h, const float *d_out, double lr, void *cuda_stream);
 

@@ -12,7 +12,9 @@
 //    RCH .cs streaming stores per batch;
 //  * other tiles: the warp walks the flattened occurrence range of its 32 bags in batches of RCH
 //    rows (keys of the next batch prefetched), accumulating in fp64 and flushing each bag at its end.
-// One tile per warp (grid-stride loop kept for very large batches).
+// One tile per warp (grid-stride loop kept for very large batches). Row loads are unconditional (a
+// missing row reads row 0 and is zeroed before use): predicated loads each hold one of the 7
+// predicate registers and ptxas then issued them in groups of ~4 instead of RCH at once.
 #include <stdlib.h>
 
 #include "common.cuh"

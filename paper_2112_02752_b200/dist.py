@@ -1,6 +1,7 @@
 """torch.distributed plumbing for the row-sharded (world > 1) mode: rank discovery from the torchrun
 environment, the 128-byte ncclUniqueId broadcast that emb_create needs, and max-over-ranks timing.
-Plumbing only: all exchanges of the embedding step run inside libemb over NCCL."""
+Plumbing only: all exchanges of the embedding step run inside libemb (peer-memory kernels; NCCL only
+bootstraps the CUDA IPC handles at create, or carries the v1 exchange when EMB_EXCHANGE=nccl)."""
 from __future__ import annotations
 
 import os
