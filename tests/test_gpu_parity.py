@@ -203,6 +203,14 @@ def test_one_id_repeated_many_times(torch):
     _edge_run(torch, wl, _hand_batch(ids, offs, B, 1, 16), steps=2)
 
 
+@pytest.mark.parametrize("opt", ["adagrad", "rowwise_adagrad"])
+def test_single_row_tables(torch, opt):
+    """Degenerate tables: one with a single row (every id is 0: one segment holding all of its
+    occurrences; 1-bit keys, one radix pass) next to a 7-row table, Zipf ids, empty bags."""
+    wl = synthgen.WORKLOADS["C1"].with_(rows=(1, 7), slot_table=(0, 1), dim=16, opt=opt, ids="zipf", zipf_s=1.1)
+    _parity_run(torch, wl, 300, steps=3, lr=0.05, empty_frac=0.1)
+
+
 def test_all_empty_bags_and_max_id(torch):
     wl = synthgen.WORKLOADS["C1"].with_(rows=(10, 5), slot_table=(0, 1), dim=8, opt="sgd")
     ids = np.array([9, 4, 4, 0])
