@@ -261,9 +261,20 @@ def main():
                        device=local_rank)
     stream = torch.cuda.current_stream()
 
+    use_prefetch = bool(os.environ.get("EMB_BENCH_PREFETCH"))  # experiment (measured slower)
+
+    def prefetch_next(i):
+        # pipelining (W = 1): the dedup sort of step i+1 enqueued before step i's backward
+        # (emb_lookup_prefetch). Off by default: the persistent gradient kernel holds the shared memory
+        # the sort needs, so the sort waits for it and the step got slower (140 -> 146 us)
+        if use_prefetch:
+            nx = dev_batches[(i + 1) % POOL_BATCHES]
+            layer.lookup_prefetch(nx.ids, nx.offsets, nx.batch, nx.nnz, stream)
+
     def step(i):
         db = dev_batches[i % POOL_BATCHES]
         layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
+        prefetch_next(i)
         layer.backward_update(db.dy, wl.lr, stream)
 
     def barrier():
@@ -308,6 +319,7 @@ def main():
             layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
             if rec:
                 fwd_ev[-1][1].record(stream)
+            prefetch_next(i)
             layer.backward_update(db.dy, wl.lr, stream)
         ev1.record(stream)
         torch.cuda.synchronize()

@@ -122,6 +122,16 @@ emb_status_t emb_get_unique_id(void *out128);
 emb_status_t emb_lookup(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                         int64_t nnz, float *out, void *cuda_stream);
 
+/* Optional pipelining (world == 1 with a monotone slot -> table map; a no-op returning EMB_OK
+ * otherwise): start the per-table dedup sort of the NEXT emb_lookup's inputs on the library's internal
+ * stream, ordered after the work already enqueued on cuda_stream (so the inputs must be ready there)
+ * but not after work enqueued later. Called between emb_lookup(k) and emb_backward_update(k), the
+ * sort of step k+1 overlaps the gradient pass of step k. The next emb_lookup consumes it when it is
+ * called with the same ids / offsets pointers and batch / nnz (any other call discards it); ids and
+ * offsets must stay valid and unmodified until then. Results are identical with or without it. */
+emb_status_t emb_lookup_prefetch(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
+                                 int64_t nnz, void *cuda_stream);
+
 /* Backward + update for the last lookup: c_j = d_out[b][s][:] (mean: / |bag|), G[g] = sum of c_j over
  * all occurrences of all ranks (fp64 accumulation, deterministic order), then one SGD or element-wise
  * Adagrad (or row-wise Adagrad) update per touched row (R8-R14'). d_out: device fp32 [batch][S][D], 16-byte aligned.

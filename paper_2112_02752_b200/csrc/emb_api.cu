@@ -77,6 +77,17 @@ struct emb_ctx {
   // ---- workspace
   std::vector<void *> allocs;
   uint32_t *key_csr = nullptr, *drow = nullptr, *k0 = nullptr, *v0 = nullptr, *k1 = nullptr, *v1 = nullptr;
+  // W = 1 sort output, two sets: a prefetched sort of the next step (emb_lookup_prefetch) writes the
+  // set the pending backward does not read
+  uint32_t *sk_set[2] = {nullptr, nullptr}, *sp_set[2] = {nullptr, nullptr}, *sort_scratch = nullptr;
+  int cur_set = 0;
+  struct {
+    bool valid = false;
+    const int64_t *ids = nullptr, *offsets = nullptr;
+    int32_t batch = 0;
+    int64_t nnz = 0;
+    int set = 0;
+  } pf;
   int32_t *blen = nullptr;
   SortWorkspace sws{};
   double *partials = nullptr;
@@ -126,7 +137,7 @@ struct emb_ctx {
 
   // ---- streams / step state
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_pf = nullptr;
   int state = 0;  // 0 idle, 1 looked up
   int32_t batch = 0;
   int64_t nnz = 0;
@@ -402,6 +413,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   }
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_pf, cudaEventDisableTiming));
   CUDA_TRY(h, launch_init(h->w, h->a, h->opt == EMB_OPT_ROWWISE_ADAGRAD, h->rows_local, h->D, h->seed,
                           h->init_accum, ks, h->rank, h->side));
 
@@ -424,6 +436,11 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   bad |= dalloc(h, &h->drow, N) != cudaSuccess;
   bad |= dalloc(h, &h->k0, N) != cudaSuccess;
   bad |= dalloc(h, &h->v0, N) != cudaSuccess;
+  if (h->world == 1) {
+    bad |= dalloc(h, &h->sk_set[1], N) != cudaSuccess;
+    bad |= dalloc(h, &h->sp_set[1], N) != cudaSuccess;
+    bad |= dalloc(h, &h->sort_scratch, N) != cudaSuccess;
+  }
   bad |= dalloc(h, &h->k1, N) != cudaSuccess;
   bad |= dalloc(h, &h->v1, N) != cudaSuccess;
   bad |= dalloc(h, &h->blen, SB) != cudaSuccess;
@@ -467,6 +484,8 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
     bad |= dalloc(h, &h->tcnt, (size_t)((N + 2047) / 2048 + 1) * EMB_MAX_WORLD) != cudaSuccess;
   }
   if (bad) return fail(h, EMB_ERR_NOMEM, "cannot allocate the step workspace");
+  h->sk_set[0] = h->k0;
+  h->sp_set[0] = h->v0;
   h->sws.hist = sort_words;
   h->sws.counters = sort_words + 4 * 256;
   h->sws.status = sort_words + 4 * 256 + 4;
@@ -557,6 +576,7 @@ void destroy_impl(emb_ctx *h) {
   for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_pf) cudaEventDestroy(h->ev_pf);
   if (h->side) cudaStreamDestroy(h->side);
   delete h;
 }
@@ -588,6 +608,56 @@ emb_status_t exchange(emb_ctx *h, const void *sendbuf, const int64_t *scnt, cons
   NCCL_TRY(h, ncclGroupEnd());
   prof_hook(h, KID_NCCL, 1, st);
   ++h->launches;
+  return EMB_OK;
+}
+
+// per-table sort arguments (W = 1 path) writing sort-output set `set`
+SegSortArgs segsort_args(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz, int set) {
+  SegSortArgs sa{};
+  sa.ids = ids;
+  sa.offsets = offsets;
+  sa.nnz = nnz;
+  sa.batch = batch;
+  sa.gslot = h->d_gslot;
+  sa.gbase = h->d_gbase;
+  sa.grows = h->d_grows;
+  sa.gbits = h->d_gbits;
+  sa.skey = h->sk_set[set];
+  sa.spay = h->sp_set[set];
+  sa.scratch_k = h->k1;
+  sa.scratch_a = h->v1;
+  sa.scratch_b = h->sort_scratch;
+  sa.run_k = h->run_k;
+  sa.run_i = h->run_i;
+  sa.K = h->segK;
+  sa.err = h->err_dev;
+  sa.err_host = h->err_host_dev;
+  sa.fin = nullptr;
+  return sa;
+}
+
+emb_status_t lookup_prefetch_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch,
+                                  int64_t nnz, cudaStream_t st) {
+  if (batch < 0 || batch > h->max_batch || nnz < 0 || nnz > h->max_ids || (batch == 0 && nnz != 0))
+    return fail(h, EMB_ERR_INVALID, "prefetch: batch / nnz out of range");
+  if ((batch > 0 && !offsets) || (nnz > 0 && !ids)) return fail(h, EMB_ERR_INVALID, "prefetch: NULL ids/offsets");
+  h->pf.valid = false;
+  if (h->world != 1 || !h->segsort_ok || batch == 0 || nnz == 0) return EMB_OK;  // nothing to overlap
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  // ordered after everything already on the caller stream (the inputs, the current lookup), not after
+  // the backward the caller enqueues next: the sort of step k+1 overlaps the gradient pass of step k.
+  // It writes the sort-output set the pending backward does not read.
+  CUDA_TRY(h, cudaEventRecord(h->ev_pf, st));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_pf, 0));
+  const int set = h->cur_set ^ 1;
+  SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, set);
+  LAUNCH(h, KID_SORT_PASS, h->side, launch_segsort(sa, h->G, h->side));
+  h->pf.valid = true;
+  h->pf.ids = ids;
+  h->pf.offsets = offsets;
+  h->pf.batch = batch;
+  h->pf.nnz = nnz;
+  h->pf.set = set;
   return EMB_OK;
 }
 
@@ -652,29 +722,21 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     // fork: the sort runs on the side stream while the pool streams rows on the caller stream
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-    if (h->segsort_ok) {
-      SegSortArgs sa{};
-      sa.ids = ids;
-      sa.offsets = offsets;
-      sa.nnz = nnz;
-      sa.batch = batch;
-      sa.gslot = h->d_gslot;
-      sa.gbase = h->d_gbase;
-      sa.grows = h->d_grows;
-      sa.gbits = h->d_gbits;
-      sa.skey = h->k0;
-      sa.spay = h->v0;
-      sa.scratch_k = h->k1;
-      sa.scratch_a = h->v1;
-      sa.scratch_b = h->useg;  // free during the forward (the unique arrays are only filled on demand)
-      sa.run_k = h->run_k;
-      sa.run_i = h->run_i;
-      sa.K = h->segK;
-      sa.err = h->err_dev;
-      sa.err_host = h->err_host_dev;
+    // a sort prefetched for exactly these inputs (emb_lookup_prefetch) is already queued on the side
+    // stream: consume it (the join below waits for it)
+    const bool use_pf = h->pf.valid && h->pf.ids == ids && h->pf.offsets == offsets && h->pf.batch == batch &&
+                        h->pf.nnz == nnz;
+    h->pf.valid = false;
+    if (use_pf) {
+      h->cur_set = h->pf.set;
+      h->skey = h->sk_set[h->cur_set];
+      h->spay = h->sp_set[h->cur_set];
+    } else if (h->segsort_ok) {
+      h->cur_set ^= 1;  // (stream-ordered after the previous backward: either set is free)
+      SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, h->cur_set);
       sa.fin = (batch > 0 && nnz > 0) ? h->fin : nullptr;  // the later of sort / pool publishes the error word
-      h->skey = h->k0;
-      h->spay = h->v0;
+      h->skey = sa.skey;
+      h->spay = sa.spay;
       static int serial = -1;  // experiment knob: EMB_SERIAL=1 runs the sort before the pool (no overlap)
       if (serial < 0) serial = getenv("EMB_SERIAL") ? atoi(getenv("EMB_SERIAL")) : 0;
       cudaStream_t ss = serial ? st : h->side;
@@ -691,7 +753,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     pa.row_idx = nullptr;
     const bool fused_pub = h->segsort_ok && batch > 0 && nnz > 0;
     pa.fin = fused_pub ? h->fin : nullptr;
-    pa.fin_kernels = 2;
+    pa.fin_kernels = use_pf ? 1 : 2;  // a prefetched sort does not take part in the publish
     if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
     CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
@@ -1072,6 +1134,12 @@ emb_status_t emb_lookup(emb_handle_t h, const int64_t *ids, const int64_t *offse
                         float *out, void *cuda_stream) {
   if (!h) return EMB_ERR_INVALID;
   return lookup_impl(h, ids, offsets, batch, nnz, out, static_cast<cudaStream_t>(cuda_stream));
+}
+
+emb_status_t emb_lookup_prefetch(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
+                                 int64_t nnz, void *cuda_stream) {
+  if (!h) return EMB_ERR_INVALID;
+  return lookup_prefetch_impl(h, ids, offsets, batch, nnz, static_cast<cudaStream_t>(cuda_stream));
 }
 
 emb_status_t emb_backward_update(emb_handle_t h, const float *d_out, double lr, void *cuda_stream) {

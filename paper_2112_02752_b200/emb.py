@@ -27,7 +27,8 @@ SHARD = {"cyclic": 0, "block": 1}
 
 # every symbol include/emb.h declares (checked by tests/test_abi.py)
 EXPORTED = [
-    "emb_create", "emb_destroy", "emb_get_unique_id", "emb_lookup", "emb_backward_update", "emb_lookup_host",
+    "emb_create", "emb_destroy", "emb_get_unique_id", "emb_lookup", "emb_lookup_prefetch", "emb_backward_update",
+    "emb_lookup_host",
     "emb_backward_update_host", "emb_read_rows", "emb_write_rows", "emb_last_step_info", "emb_last_unique",
     "emb_last_owner_unique", "emb_rows_local", "emb_profile_enable", "emb_profile_reset", "emb_profile_read",
     "emb_profile_name", "emb_clear_error", "emb_last_error",
@@ -80,6 +81,7 @@ def lib() -> ctypes.CDLL:
     L.emb_destroy.argtypes = [vp]
     L.emb_get_unique_id.argtypes = [vp]
     L.emb_lookup.argtypes = [vp, vp, vp, i32, i64, vp, vp]
+    L.emb_lookup_prefetch.argtypes = [vp, vp, vp, i32, i64, vp]
     L.emb_backward_update.argtypes = [vp, vp, ctypes.c_double, vp]
     L.emb_lookup_host.argtypes = [vp, vp, vp, i32, i64, vp, vp]
     L.emb_backward_update_host.argtypes = [vp, vp, ctypes.c_double, vp]
@@ -192,6 +194,11 @@ class EmbeddingLayer:
     def lookup(self, ids, offsets, batch: int, nnz: int, out, stream=None):
         self._check(lib().emb_lookup(self.h, _ptr(ids), _ptr(offsets), int(batch), int(nnz), _ptr(out),
                                      _stream(stream, self.device)), "emb_lookup")
+
+    def lookup_prefetch(self, ids, offsets, batch: int, nnz: int, stream=None):
+        """Start the dedup sort of the NEXT lookup's inputs so it overlaps this step's backward (W = 1)."""
+        self._check(lib().emb_lookup_prefetch(self.h, _ptr(ids), _ptr(offsets), int(batch), int(nnz),
+                                              _stream(stream, self.device)), "emb_lookup_prefetch")
 
     def backward_update(self, d_out, lr: float, stream=None):
         self._check(lib().emb_backward_update(self.h, _ptr(d_out), float(lr), _stream(stream, self.device)),
