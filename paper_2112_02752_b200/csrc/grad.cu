@@ -25,9 +25,11 @@
 //    LAST arriving warp sums the partials in warp order and applies. Warp order is fixed, so the
 //    results are bitwise reproducible run to run (R10).
 // Sinks (template MODE): 0 = SGD: w <- w - lr*G in fp64, rounded once (as the oracle). 1 = Adagrad
-// (element-wise, eps outside the sqrt, R12): a <- a + G^2 in fp64 rounded to fp32; the update
-// lr*G/(sqrt(a)+eps) in fp32 with MUFU sqrt/rcp (|update| <= lr, so its relative error of a few
-// 1e-7 is <= 1e-8 absolute, far inside the 1e-6 + 1e-5|w| tolerance; DESIGN.md §3 R16').
+// (element-wise, eps outside the sqrt, R12): a <- fma(g, g, a) in fp32 with g = fp32(G) (relative
+// error <= ~2e-7 against the oracle's fp64 a + G^2 rounded once; the fp64 form cost 4 us per step in
+// conversions); the update lr*g/(sqrt(a)+eps) in fp32 with MUFU sqrt/rcp (|update| <= lr, so its
+// relative error of a few 1e-7 is <= 1e-8 absolute, far inside the 1e-6 + 1e-5|w| tolerance;
+// DESIGN.md §2 R16').
 // 2 = write the fp32 per-unique-key gradient (requester side of the W>1 exchange). 3 = the same row
 // stored into the owner through peer memory. 4 = row-wise Adagrad (SURVEY §8(f) f1, R14'): one
 // accumulator per row, a <- a + (1/D) sum_c G[c]^2 (fp64 xor-butterfly warp reduction: every lane
@@ -97,9 +99,8 @@ __device__ __forceinline__ void apply_frag(const GradArgs &a, const OptConst &oc
     VecF<CPL> ao;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
-      const double a64 = __dadd_rn((double)av.v[c], __dmul_rn(acc[c], acc[c]));
-      const float af = (float)a64;
       const float g = (float)acc[c];
+      const float af = __fmaf_rn(g, g, av.v[c]);  // a + G^2: one fp32 FMA from the rounded G (R16')
       const float r = rcp_approx(sqrt_approx(af) + oc.epsf);
       ao.v[c] = af;
       wo.v[c] = wv.v[c] - (oc.lrf * g) * r;
