@@ -388,7 +388,7 @@ def main():
                "path": "emb_lookup_host + emb_backward_update_host (pinned host buffers)"}
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and n == 1 and not args.no_cpu:  # the CPU baseline is an N = 1 figure
         sps, lps, sample = oracle_time(wl, budget_s=args.cpu_budget)
         thr, pool = cpu_threads()
         cpu = {"value": sps, "unit": "samples/s", "cores": thr, "kind": "oracle",
