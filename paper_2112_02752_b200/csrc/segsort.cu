@@ -16,8 +16,9 @@
 //  * the compacted items (local id, occurrence index) are sorted with a stable LSD radix sort on the
 //    group's key bits (24 bits = 3 passes of 8 for a 10M-row table): per pass, per-warp digit counts
 //    (shared-memory atomics over the warp's contiguous sub-chunk), a digit-major scan of the
-//    (digit, warp) counters, then a stable scatter ranked by a warp multisplit (peer masks from 8
-//    ballots per 32-item row);
+//    (digit, warp) counters, then a stable scatter ranked by a warp multisplit (peer masks from one
+//    MATCH.ANY per 32-item row; 8 ballots before: sort alone 40 -> 37 us, step time unchanged because
+//    the concurrent pool then takes the freed issue slots);
 //  * items are written straight to their final sorted positions: no merge.
 // Ranges above SEG_CHUNK_CAP items run the same code on global scratch (correct, slower). Invalid
 // occurrences (EMB_SENTINEL) get local key rows[t] and sort to the end of their group.
@@ -25,6 +26,10 @@
 
 #include "common.cuh"
 #include "internal.h"
+
+#ifndef EMB_SEG_MATCH
+#define EMB_SEG_MATCH 1
+#endif
 
 namespace emb {
 
@@ -36,6 +41,11 @@ constexpr uint32_t SEG_CHUNK_CAP = 8192;  // items per range sorted in shared me
 
 // lanes of the warp holding the same 8-bit digit as this lane (8 ballots)
 __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
+#if EMB_SEG_MATCH
+  // one MATCH.ANY instead of 8 ballots (invalid lanes get a value no valid lane has)
+  const uint32_t m = __match_any_sync(0xffffffffu, valid ? d : 0x100u + (threadIdx.x & 31));
+  return valid ? m : 0u;
+#else
   uint32_t m = __ballot_sync(0xffffffffu, valid);
   if (!valid) m = 0;
 #pragma unroll
@@ -44,6 +54,7 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
     m &= ((d >> b) & 1u) ? bb : ~bb;
   }
   return m;
+#endif
 }
 
 __device__ __forceinline__ void group_bounds(const SegSortArgs &a, int g, int64_t &lo, int64_t &hi) {
