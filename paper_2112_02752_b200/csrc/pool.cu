@@ -8,8 +8,8 @@
 // one 256-B coalesced row per instruction) and a tile of 32 consecutive bags (slot-major CSR: one
 // slot's consecutive samples), lane l holding bag l's CSR bounds and output row b*S+s (32-bit math).
 //  * tiles of single-id bags (the Criteo case): the 32 keys are fetched in one coalesced load and
-//    each lane then issues RCH = 32/CPL independent row loads (ld.global.nc, L1 no-allocate) and
-//    RCH .cs streaming stores per batch;
+//    each lane then issues RCH independent row loads (ld.global.nc, L1 no-allocate; RCH = 32 at
+//    D <= 64, i.e. the whole tile in flight) and RCH .cs streaming stores per batch;
 //  * other tiles: the warp walks the flattened occurrence range of its 32 bags in batches of RCH
 //    rows (keys of the next batch prefetched), accumulating in fp64 and flushing each bag at its end.
 // One tile per warp (grid-stride loop kept for very large batches). Row loads are unconditional (a
@@ -226,9 +226,11 @@ cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st) {
   if (a.dim <= 64) {
     if (var == 1) return launch_pool_t<2, 32, 2>(a, ntiles, st);
     if (var == 7) return launch_pool_t<2, 16, 2>(a, ntiles, st);
-    if (var == 2) return launch_pool_t<2, 32, 3>(a, ntiles, st);
+    if (var == 2) return launch_pool_t<2, 16, 3>(a, ntiles, st);
     if (var == 3) return launch_pool_t<2, 8, 4>(a, ntiles, st);
-    return launch_pool_t<2, 16, 3>(a, ntiles, st);
+    // all 32 rows of a tile in flight per lane (registers allow it now that the loads are
+    // unconditional): C2 step 136.6 -> 133.5 us against 16 rows
+    return launch_pool_t<2, 32, 3>(a, ntiles, st);
   }
   if (a.dim <= 128) return launch_pool_t<4, 8, 3>(a, ntiles, st);
   return launch_pool_t<8, 4, 3>(a, ntiles, st);
