@@ -141,13 +141,16 @@ __device__ __forceinline__ void apply_rowwise(const GradArgs &a, const OptConst 
 
 // destination row of a merged per-key gradient (MODE 2: local X3 send buffer; MODE 3: the owner's
 // receive buffer through peer memory, at my offset there + the key's position in my send order)
+// MODE 3: the route table's send offsets / destination offsets, staged in shared memory once per CTA
+// (the per-row owner search then reads shared memory, not a chain of global loads)
+__shared__ int64_t g_rt_soff[P2P_MAXW + 1], g_rt_dst[P2P_MAXW];
+
 template <int MODE>
 __device__ __forceinline__ float *out_row(const GradArgs &a, uint32_t ui, int D) {
   if constexpr (MODE == 3) {
-    const RouteTable *rt = a.p2p.rt;
     int d = 0;
-    while (d + 1 < a.p2p.world && (int64_t)ui >= rt->soff[d + 1]) ++d;
-    return a.p2p.peer_grecv[d] + (size_t)(rt->dst_off[d] + ((int64_t)ui - rt->soff[d])) * D;
+    while (d + 1 < a.p2p.world && (int64_t)ui >= g_rt_soff[d + 1]) ++d;
+    return a.p2p.peer_grecv[d] + (size_t)(g_rt_dst[d] + ((int64_t)ui - g_rt_soff[d])) * D;
   } else {
     return a.out_rows + (size_t)ui * D;
   }
@@ -284,6 +287,11 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
   const int C16 = D >> 2;  // 16-byte chunks per row (a constant when DC != 0)
   const size_t stage_floats = (size_t)NA * T * D + (MODE == 4 ? T : 0);  // (+ T row accumulators)
   const uint32_t wbase = smem_u32(smem) + (uint32_t)(wib * NS * stage_floats * 4);
+  if constexpr (MODE == 3) {
+    if (threadIdx.x <= a.p2p.world) g_rt_soff[threadIdx.x] = a.p2p.rt->soff[threadIdx.x];
+    if (threadIdx.x < a.p2p.world) g_rt_dst[threadIdx.x] = a.p2p.rt->dst_off[threadIdx.x];
+    __syncthreads();
+  }
   const int64_t gw = ((int64_t)blockIdx.x * (blockDim.x >> 5)) + wib;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t n = a.n_dev ? *a.n_dev : a.n;
