@@ -117,6 +117,8 @@ def main():
         if info["recv_counts"] != [recv[r][rank] for r in range(world)]:
             ok = False
             msgs.append(f"step {s}: recv counts inconsistent")
+        if case == "c3":  # emb_lookup_prefetch is a documented no-op at W > 1: results must not change
+            layer.lookup_prefetch(db.ids, db.offsets, db.batch, db.nnz)
         layer.backward_update(db.dy, wl.lr)
         torch.cuda.synchronize()
         ora.backward_update([b.dy for b in batch_list], wl.lr)
