@@ -32,8 +32,8 @@
 // DESIGN.md §2 R16').
 // 2 = write the fp32 per-unique-key gradient (requester side of the W>1 exchange). 3 = the same row
 // stored into the owner through peer memory. 4 = row-wise Adagrad (SURVEY §8(f) f1, R14'): one
-// accumulator per row, a <- a + (1/D) sum_c G[c]^2 (fp64 xor-butterfly warp reduction: every lane
-// ends with the same total) rounded to fp32; w as in mode 1 with the row's a.
+// accumulator per row, a <- a + (1/D) sum_c g[c]^2 with g = fp32(G) (fp32 FMAs + an xor-butterfly
+// warp reduction: every lane ends with the same total); w as in mode 1 with the row's a.
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -116,24 +116,27 @@ template <int CPL>
 __device__ __forceinline__ void apply_rowwise(const GradArgs &a, const OptConst &oc, const double (&acc)[CPL],
                                               const VecF<CPL> &wv, float a_old, size_t row_off, uint32_t lrow,
                                               bool active, int D) {
-  double s = 0.0;
-  if (active) {
+  // the row's sum of squares in fp32 from the rounded gradient g = fp32(G) (the g the update uses):
+  // FMAs per lane, then an xor butterfly -- at every level the two partners add the same two operands
+  // (commutative), so all lanes end with the bitwise identical total. Relative error <= ~4e-7 against
+  // the oracle's fp64 mean of G^2 (reading R14'); the fp64 chain cost ~20 us of the C2 step.
+  VecF<CPL> g;
+  float s = 0.f;
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) s = __dadd_rn(s, __dmul_rn(acc[c], acc[c]));
+  for (int c = 0; c < CPL; ++c) {
+    g.v[c] = (float)acc[c];
+    if (active) s = __fmaf_rn(g.v[c], g.v[c], s);
   }
-  // xor butterfly: at every level the two partners add the same two operands (commutative), so all
-  // lanes end with the bitwise identical total
 #pragma unroll
-  for (int o = 16; o; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  for (int o = 16; o; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
   // s / D: a multiply by the exact reciprocal when D is a power of two (every configured D)
-  const double mean = (D & (D - 1)) == 0 ? __dmul_rn(s, 1.0 / (double)D) : __ddiv_rn(s, (double)D);
-  const double a64 = __dadd_rn((double)a_old, mean);
-  const float af = (float)a64;
+  const float mean = (D & (D - 1)) == 0 ? __fmul_rn(s, 1.0f / (float)D) : __fdiv_rn(s, (float)D);
+  const float af = __fadd_rn(a_old, mean);
   const float r = rcp_approx(sqrt_approx(af) + oc.epsf);
   if (active) {
     VecF<CPL> wo;
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) wo.v[c] = wv.v[c] - (oc.lrf * (float)acc[c]) * r;
+    for (int c = 0; c < CPL; ++c) wo.v[c] = wv.v[c] - (oc.lrf * g.v[c]) * r;
     stg_frag<CPL>(a.w + row_off, wo);
   }
   if ((threadIdx.x & 31) == 0) a.a[lrow] = af;
