@@ -23,10 +23,18 @@
  *    device detects (id < 0 or id >= rows[t]: EMB_ERR_RANGE; non-monotone offsets or offsets[S*B] !=
  *    nnz: EMB_ERR_INVALID) set a sticky flag; an offending id contributes nothing and updates
  *    nothing; the flag is returned by the next API call after the device work completed, and stays
- *    set until emb_clear_error(). emb_last_error() gives a text. No call ever aborts the process.
+ *    set until emb_clear_error(). The update of a step whose input had an error is skipped entirely
+ *    (decided on the device, so it does not depend on host timing). emb_last_error() gives a text.
+ *    No call ever aborts the process.
  *  - Step protocol: emb_lookup, then exactly one emb_backward_update (else EMB_ERR_STATE); one host
  *    thread per handle. With world > 1 every rank makes the same sequence of lookup/backward calls
  *    (they are collective); per-rank batch sizes may differ.
+ *  - Errors at world > 1: a lookup / backward call always takes part in the collective step, even
+ *    with bad arguments (the rank then contributes an empty batch and returns EMB_ERR_INVALID). A step
+ *    in which ANY rank had an input error (bad arguments, an id out of range, bad offsets, or a sticky
+ *    error not yet cleared) updates no row on any rank; forward outputs of valid bags are still
+ *    computed. A rank that skips a collective call makes its peers' waits time out after ~4 s: they
+ *    report EMB_ERR_NCCL (sticky) and skip the work; the handles must then be recreated.
  *  - Sharding (R7): fused row space g = base[t] + id, base[t] = sum_{t'<t} rows[t']. CYCLIC: owner(g)
  *    = g mod W, local(g) = g div W. BLOCK: rows_per = ceil(R_total/W), owner = g div rows_per, local =
  *    g mod rows_per. Requires R_total < 2^32 and (for W > 1) the routing key owner*2^b + local < 2^32.
@@ -54,7 +62,7 @@ typedef enum {
   EMB_ERR_STATE = 3,   /* backward without lookup, double lookup, unsupported call in this state */
   EMB_ERR_NOMEM = 4,   /* device or pinned-host allocation failed in emb_create                   */
   EMB_ERR_CUDA = 5,    /* a CUDA runtime call failed                                              */
-  EMB_ERR_NCCL = 6     /* NCCL failed or is unavailable                                           */
+  EMB_ERR_NCCL = 6     /* NCCL bootstrap failed, or a peer never arrived at an exchange (timeout) */
 } emb_status_t;
 
 typedef enum { EMB_POOL_SUM = 0, EMB_POOL_MEAN = 1 } emb_pool_t;          /* R1 */
@@ -78,7 +86,10 @@ typedef struct {
   int64_t max_ids;          /* per-rank per-step capacity nnz_max >= 1                       */
   int32_t rank;             /* 0 <= rank < world                                             */
   int32_t world;            /* 1 <= world <= EMB_MAX_WORLD                                   */
-  const void *nccl_id;      /* host, 128-byte ncclUniqueId from emb_get_unique_id on rank 0; required iff world > 1 */
+  const void *nccl_id;      /* host, 128-byte ncclUniqueId from emb_get_unique_id on rank 0; required iff
+                               world > 1 and the handle is created with emb_create (one rank per
+                               process; NCCL only bootstraps the peer mappings); ignored by
+                               emb_create_group */
   int32_t device;           /* CUDA device ordinal used by this handle                       */
   int32_t shard;            /* emb_shard_t                                                   */
 } emb_config_t;
@@ -91,7 +102,7 @@ typedef struct {
   int64_t unique_owner;                  /* U_o: distinct rows this rank owns that were requested (W>1; = U_l at W=1) */
   int64_t recv_keys;                     /* keys received from all ranks (W>1; = U_l at W=1)       */
   int32_t world;
-  int32_t launches;                      /* kernels + NCCL calls enqueued by the last lookup+backward */
+  int32_t launches;                      /* kernels enqueued by the last lookup+backward            */
   int64_t send_counts[EMB_MAX_WORLD];    /* keys sent to each owner                                 */
   int64_t recv_counts[EMB_MAX_WORLD];    /* keys received from each requester                       */
 } emb_step_info_t;
@@ -100,9 +111,20 @@ typedef struct {
 
 /* Create a handle: validates cfg, selects cfg->device, allocates the fp32 shard [rows_local][D]
  * (+ the Adagrad accumulator), initialises it with the R15 hash, sizes the workspace from
- * max_batch / max_ids / world. Collective across ranks when world > 1 (ncclCommInitRank).
- * Synchronous. On failure *out is NULL. */
+ * max_batch / max_ids / world. world > 1 (one rank per process, all on one host): collective across
+ * ranks -- ncclCommInitRank, an all-gather of max_ids and the GPUs' PCI ids (every rank must have peer
+ * access to every other rank's GPU, else EMB_ERR_INVALID), then an all-gather of CUDA IPC handles of
+ * the exchange buffers and table shards. Synchronous. On failure *out is NULL. */
 emb_status_t emb_create(const emb_config_t *cfg, emb_handle_t *out);
+
+/* Create ALL n = world ranks of a row-sharded layer in this process (group mode): cfgs[r] has
+ * world == n and rank == r; devices may differ (peer access is enabled between them) or coincide
+ * (several ranks emulated on one GPU). out: host array [n] of handles. The ranks step together
+ * through emb_lookup_group / emb_backward_update_group only (emb_lookup on a group handle returns
+ * EMB_ERR_STATE). Every kernel of the exchange is the one a multi-process rank runs; the group calls
+ * order the ranks' phases with cross-stream events, so no kernel waits on a kernel that is not
+ * already complete. Destroy each handle with emb_destroy. */
+emb_status_t emb_create_group(const emb_config_t *cfgs, int32_t n, emb_handle_t *out);
 
 /* Free everything the handle owns (synchronises its streams). NULL is a no-op. */
 emb_status_t emb_destroy(emb_handle_t h);
@@ -115,10 +137,10 @@ emb_status_t emb_get_unique_id(void *out128);
 /* Forward: out[b][s][:] = sum (or mean) over bag (s,b) of W_t[id][:]  (R1-R5).
  * ids: device int64 [nnz]; offsets: device int64 [S*batch+1]; out: device fp32 [batch][S][D],
  * 16-byte aligned. 0 <= batch <= max_batch, 0 <= nnz <= max_ids. Also dedups the ids per rank and,
- * when world > 1, routes the unique keys to their owners and returns the rows (collective: device-side
- * exchange over NVLink peer memory, or NCCL grouped send/recv with one host wait for the per-peer
- * counts when EMB_EXCHANGE=nccl or the slot -> table map is not monotone). Saves what backward needs
- * in the workspace, so ids and offsets may be reused once the stream work completes. */
+ * when world > 1, routes the distinct keys to their owners and pulls the remote distinct rows from
+ * the owners' shards (collective; device-side exchange over NVLink peer memory, no host
+ * synchronisation). Saves what backward needs in the workspace, so ids and offsets may be reused once
+ * the stream work completes. */
 emb_status_t emb_lookup(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                         int64_t nnz, float *out, void *cuda_stream);
 
@@ -135,8 +157,19 @@ emb_status_t emb_lookup_prefetch(emb_handle_t h, const int64_t *ids, const int64
 /* Backward + update for the last lookup: c_j = d_out[b][s][:] (mean: / |bag|), G[g] = sum of c_j over
  * all occurrences of all ranks (fp64 accumulation, deterministic order), then one SGD or element-wise
  * Adagrad (or row-wise Adagrad) update per touched row (R8-R14'). d_out: device fp32 [batch][S][D], 16-byte aligned.
- * Collective when world > 1. */
+ * Collective when world > 1: the merged per-key gradients go to the rows' owners, which merge the
+ * ranks' contributions in source-rank order and apply. */
 emb_status_t emb_backward_update(emb_handle_t h, const float *d_out, double lr, void *cuda_stream);
+
+/* Group-mode step over all n ranks (handles from emb_create_group, in rank order). Per rank r the
+ * arguments mean what they mean for emb_lookup / emb_backward_update; ids, offsets, batch, nnz, out,
+ * d_out are host arrays [n] of per-rank values; streams: host array [n] of cudaStream_t on each rank's
+ * device (NULL = the legacy default stream for every rank). Returns the first error of any rank (the
+ * other ranks' calls still took part, see "Errors at world > 1"). */
+emb_status_t emb_lookup_group(emb_handle_t *hs, int32_t n, const int64_t *const *ids, const int64_t *const *offsets,
+                              const int32_t *batch, const int64_t *nnz, float *const *out, void *const *streams);
+emb_status_t emb_backward_update_group(emb_handle_t *hs, int32_t n, const float *const *d_out, double lr,
+                                       void *const *streams);
 
 /* End-to-end variants over HOST buffers (pinned recommended): copy the inputs host->device, run the
  * device call above on cuda_stream, copy the result device->host, and return after the stream work

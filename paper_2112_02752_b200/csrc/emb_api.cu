@@ -1,26 +1,33 @@
 // emb_api.cu — EmbContext runtime + the C ABI of include/emb.h.
 //
 // Owns: the fp32 row shard [rows_local][D] (+ Adagrad accumulator), all step workspace (sized once
-// in emb_create from max_batch / max_ids / world), a side stream for the sort (overlapped with the
-// forward pool), the NCCL communicator for world > 1, and the step state machine.
+// in emb_create from max_batch / max_ids / world), a side stream, the peer mappings for world > 1,
+// and the step state machine.
 //
 // Step at world == 1 (no host sync):
-//   lookup   : K1 keys -> fork{ side: radix sort (key, j) } ; main: K5 pool straight from the table
-//              -> join
-//   backward : K6+K7 fused segment-reduce + optimizer apply over the sorted keys
-// Step at world > 1 (v1 exchange: grouped ncclSend/ncclRecv all-to-allv, one host sync for counts):
-//   lookup   : K1 keys (owner-major routing keys) -> sort -> unique -> per-owner counts
-//              -> X0 counts all-to-all -> host reads counts -> X1 local ids all-to-allv
-//              -> owner gather -> X2 rows all-to-allv -> K5 pool from the received unique rows;
-//              side stream: owner-side sort of the received keys (for the backward merge)
-//   backward : K6 segment reduce -> per-unique-key fp32 grads -> X3 all-to-allv to the owners
-//              -> K6+K7 owner merge (source-rank order) + optimizer apply
+//   lookup   : fork{ side: per-table dedup sort (key, occurrence) } ; main: pool straight from the
+//              table -> join
+//   backward : fused segment-reduce + optimizer apply over the sorted keys
+// Step at world > 1 (no host sync; e = the step's epoch, exchanges over peer memory, p2p.cu):
+//   lookup   : L0 sort -> k_route (keys into the owners' regions, counts + error bits, KEYS(e))
+//              L1 side: wait KEYS(e) -> owner merge of the W received runs
+//                 main: wait APPLIED(e-1) -> pull my remote distinct rows -> pool -> join
+//   backward : B0 requester merge of duplicate-id gradients, rows stored into the owners' regions
+//                 (GRADS(e))
+//              B1 wait GRADS(e) -> owner merge over sources (source-rank order) + apply (APPLIED(e))
+// Multi-process (one rank per process): a rank runs its phases back to back and the in-kernel flag
+// waits order it against its peers. Group mode (emb_create_group: all ranks in this process, any
+// devices, possibly one): emb_lookup_group / emb_backward_update_group run phase by phase over the
+// ranks with cross-stream events between phases, so every flag a wait looks at was raised by a
+// kernel that already completed -- no kernel ever waits on a kernel that may not be running.
 #include <nccl.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -36,10 +43,9 @@ namespace {
 std::mutex g_err_mu;
 std::string g_create_error = "no error";
 
-const char *kKernelNames[KID_COUNT] = {"keys",        "sort_hist",  "sort_pass", "pool",
-                                       "grad_apply",  "unique",     "route",     "owner_gather",
-                                       "grad_local",  "nccl",       "init",      "owner_merge",
-                                       "p2p_wait"};
+const char *kKernelNames[KID_COUNT] = {"keys",      "sort_hist", "sort_pass", "pool",        "grad_apply",
+                                       "unique",    "route",     "pull",      "grad_push",   "signal",
+                                       "init",      "owner_merge", "p2p_wait"};
 
 uint32_t bits_for(uint64_t x) {  // smallest b with x < 2^b (x >= 0)
   uint32_t b = 0;
@@ -64,9 +70,7 @@ struct emb_ctx {
   int32_t rank = 0, world = 1, device = 0, shard = 0;
   uint64_t R_total = 0;
   KeySpace ks{};
-  int64_t rows_local = 0, rows_local_max = 0;
-  uint32_t lmask = 0xFFFFFFFFu;
-  uint32_t owner_key_bits = 0;
+  int64_t rows_local = 0;
 
   // ---- device state
   float *w = nullptr, *a = nullptr;
@@ -92,11 +96,12 @@ struct emb_ctx {
   SortWorkspace sws{};
   double *partials = nullptr;
   uint32_t *tickets = nullptr;
+  int64_t nticket = 0;
   uint32_t *useg = nullptr, *ukey = nullptr, *ustart = nullptr, *uend = nullptr, *u_count = nullptr,
            *uniq_counter = nullptr, *fin = nullptr;
   uint64_t *uniq_status = nullptr, *ouniq_status = nullptr;
   uint32_t uniq_epoch = 0, ouniq_epoch = 0;
-  // world == 1 per-table sort (segsort.cu): table groups of the slot-major CSR
+  // per-table sort (segsort.cu): table groups of the slot-major CSR
   bool segsort_ok = false;
   int32_t G = 0, segK = 1;
   uint32_t *run_k = nullptr, *run_i = nullptr;
@@ -106,52 +111,55 @@ struct emb_ctx {
   uint32_t *err_dev = nullptr;
   uint32_t *err_host = nullptr;      // pinned, mapped
   uint32_t *err_host_dev = nullptr;  // device alias of err_host
-  // world > 1
-  uint32_t *inv = nullptr;           // [max_ids] occurrence -> unique index
-  uint32_t *send_keys = nullptr;     // [max_ids] local ids grouped by owner
-  uint32_t *recv_keys = nullptr;     // [recv_cap]
-  float *owner_rows = nullptr;       // [recv_cap][D]
-  float *uniq_rows = nullptr;        // [max_ids][D]
-  float *gloc = nullptr;             // [max_ids][D]
-  float *grecv = nullptr;            // [recv_cap][D]
-  uint32_t *ok0 = nullptr, *ov0 = nullptr, *ok1 = nullptr, *ov1 = nullptr;  // owner sort buffers
-  uint32_t *sp = nullptr, *outidx = nullptr, *tcnt = nullptr;  // owner partition (segsort path)
-  bool ukey_is_g = false;        // requester unique keys are fused keys g (segsort path) or routing keys
-  bool owner_unique_done = false;
-  uint32_t *ouseg = nullptr, *oukey = nullptr, *oustart = nullptr, *ouend = nullptr, *ou_count = nullptr,
-           *ouniq_counter = nullptr;  // owner-side dedup of the received keys
-  int64_t *d_counts = nullptr;       // [2][EMB_MAX_WORLD] send, recv
-  int64_t *h_counts = nullptr;       // pinned [2*EMB_MAX_WORLD + 1]
-  int64_t recv_cap = 0;
-  ncclComm_t comm = nullptr;
-  // peer-memory exchange (p2p.cu): IPC-mapped peer buffers, epoch flags, device route table
-  bool use_p2p = false;
+
+  // ---- world > 1 (p2p.cu / route.cu)
+  int64_t cap = 0;                   // entries per source region: max over ranks of max_ids
+  uint32_t *inv = nullptr;           // [max_ids] occurrence -> o*cap + sendpos
+  uint32_t *outidx = nullptr;        // [max_ids] sorted position -> sendpos
+  uint32_t *send_local = nullptr;    // [W*cap] my distinct keys' local ids per owner region
+  int64_t *scnt = nullptr;           // [P2P_MAXW] my per-owner counts (device)
+  uint32_t *route_tot = nullptr, *route_counter = nullptr, *route_done = nullptr;
+  uint64_t *route_status = nullptr;
+  uint32_t route_tag = 0;
+  uint32_t *recv_keys = nullptr;     // [2][W*cap] (peer-written)
+  float *uniq_rows = nullptr;        // [W*cap][D] pulled rows
+  float *grecv = nullptr;            // [2][W*cap][D] hi / lo parts (peer-written)
+  uint32_t *ok0 = nullptr, *ov0 = nullptr, *ok1 = nullptr, *ov1 = nullptr;  // owner merge
+  int64_t *n_merged = nullptr;       // device: keys received this step
+  int64_t *xmat = nullptr;           // [2][2][P2P_MAXW] (peer-written)
+  uint64_t *flags = nullptr;         // [P2P_NKIND][P2P_MAXW] (peer-written)
+  uint32_t *p2p_done = nullptr;
   P2PArgs p2p{};
   uint64_t epoch = 0;
-  int64_t *xmat = nullptr;
-  uint64_t *flags = nullptr;
-  RouteTable *rt = nullptr;
-  uint32_t *p2p_done = nullptr;
+  ncclComm_t comm = nullptr;
   std::vector<void *> ipc_opened;
+  bool group = false;                // created by emb_create_group (all ranks in this process)
   bool counts_synced = true;
+  bool owner_unique_done = false;
+  uint32_t *ouseg = nullptr, *oukey = nullptr, *oustart = nullptr, *ouend = nullptr, *ou_count = nullptr,
+           *ouniq_counter = nullptr;  // owner-side dedup of the merged keys (statistics, on demand)
+  uint32_t step_err_bits = 0;        // host-detected argument errors of the pending collective step
 
   // ---- streams / step state
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_pf = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_pf = nullptr, ev_phase = nullptr;
   int state = 0;  // 0 idle, 1 looked up
   int32_t batch = 0;
   int64_t nnz = 0;
+  const int64_t *cur_ids = nullptr, *cur_offsets = nullptr;
+  float *cur_out = nullptr;
   uint32_t *skey = nullptr, *spay = nullptr;   // requester-side sorted keys / payload of the last lookup
-  uint32_t *okey = nullptr, *opay = nullptr;   // owner-side sorted received keys / payload
   int64_t U_l = 0, n_recv = 0;
   int64_t send_counts[EMB_MAX_WORLD] = {0}, recv_counts[EMB_MAX_WORLD] = {0};
-  int64_t soff[EMB_MAX_WORLD + 1] = {0}, roff[EMB_MAX_WORLD + 1] = {0};
   cudaStream_t last_stream = nullptr;
   int launches = 0;
 
-  // ---- host-buffer (e2e) staging, allocated on first use
-  int64_t *st_ids = nullptr, *st_offsets = nullptr;
-  float *st_out = nullptr, *st_dout = nullptr;
+  // ---- host-buffer (e2e) staging, allocated on first use (two sets: double buffering)
+  int64_t *st_ids[2] = {nullptr, nullptr}, *st_offsets[2] = {nullptr, nullptr};
+  float *st_out[2] = {nullptr, nullptr}, *st_dout[2] = {nullptr, nullptr};
+  int st_set = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
 
   // ---- profiler
   bool prof_on = false;
@@ -216,7 +224,9 @@ void prof_hook(void *vctx, int kid, int end, cudaStream_t st) {
 emb_status_t check_sticky(emb_ctx *h) {
   const uint32_t e = *(volatile uint32_t *)h->err_host;
   if (e & EMB_DEVERR_TIMEOUT)
-    return fail(h, EMB_ERR_NCCL, "device: a peer never raised its exchange flag (sticky)");
+    return fail(h, EMB_ERR_NCCL,
+                "device: a peer never raised its exchange flag (sticky; a rank skipped a collective call: "
+                "recreate the handles)");
   if (e & EMB_DEVERR_INTERNAL)
     return fail(h, EMB_ERR_CUDA, "device: an internal bounds guard tripped (library bug; work was skipped)");
   if (e & EMB_DEVERR_RANGE) return fail(h, EMB_ERR_RANGE, "device: an id was < 0 or >= rows[t] (sticky)");
@@ -227,94 +237,171 @@ emb_status_t check_sticky(emb_ctx *h) {
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-int64_t owner_of_global(const emb_ctx *h, uint64_t g) {
-  if (h->world == 1) return 0;
-  return h->shard == 0 ? (int64_t)(g % (uint64_t)h->world) : (int64_t)(g / h->ks.rows_per);
-}
-int64_t local_of_global(const emb_ctx *h, uint64_t g) {
-  if (h->world == 1) return (int64_t)g;
-  return h->shard == 0 ? (int64_t)(g / (uint64_t)h->world) : (int64_t)(g % h->ks.rows_per);
-}
+int64_t owner_of_global(const emb_ctx *h, uint64_t g) { return owner_of_g((uint32_t)g, h->ks); }
+int64_t local_of_global(const emb_ctx *h, uint64_t g) { return local_of_g((uint32_t)g, h->ks); }
 
-// ------------------------------------------------------------------------------------------------
 // optimizer-state floats per row: D (element-wise Adagrad) or 1 (row-wise)
 int32_t accum_width(const emb_ctx *h) { return h->opt == EMB_OPT_ROWWISE_ADAGRAD ? 1 : h->D; }
 
-// world > 1: map every peer's exchange buffers (CUDA IPC handles all-gathered over NCCL)
-emb_status_t setup_p2p(emb_ctx *h) {
+// world > 1: the buffers peers write into / read from, in P2PArgs order
+constexpr int NB_PEER = 5;
+void peer_buffers(emb_ctx *h, void *out[NB_PEER]) {
+  out[0] = h->xmat;
+  out[1] = h->flags;
+  out[2] = h->recv_keys;
+  out[3] = h->grecv;
+  out[4] = h->w;
+}
+void set_peer(emb_ctx *h, int r, void *const ptr[NB_PEER]) {
+  P2PArgs &p = h->p2p;
+  p.peer_xmat[r] = static_cast<int64_t *>(ptr[0]);
+  p.peer_flags[r] = static_cast<uint64_t *>(ptr[1]);
+  p.peer_recv_keys[r] = static_cast<uint32_t *>(ptr[2]);
+  p.peer_grecv[r] = static_cast<float *>(ptr[3]);
+  p.peer_w[r] = static_cast<const float *>(ptr[4]);
+}
+void init_p2p_args(emb_ctx *h) {
+  P2PArgs &p = h->p2p;
+  p.world = h->world;
+  p.rank = h->rank;
+  p.cap = h->cap;
+  p.flags = h->flags;
+  p.done = h->p2p_done;
+  p.xmat = h->xmat;
+}
+
+// multi-process: before allocating, agree on the region size (max of max_ids) and check that every
+// peer GPU is reachable with peer access from this one (same host, NVLink / PCIe P2P)
+struct RankInfo {
+  int64_t max_ids;
+  uint64_t host;
+  char busid[32];
+};
+emb_status_t mp_handshake(emb_ctx *h, int64_t *cap_out) {
   const int W = h->world;
-  if (dalloc(h, &h->xmat, (size_t)P2P_MAXW * P2P_MAXW) || dalloc(h, &h->flags, (size_t)P2P_NKIND * P2P_MAXW) ||
-      dalloc(h, &h->rt, 1) || dalloc(h, &h->p2p_done, (size_t)P2P_NKIND))
-    return fail(h, EMB_ERR_NOMEM, "alloc p2p state");
-  CUDA_TRY(h, cudaMemset(h->p2p_done, 0, sizeof(uint32_t) * P2P_NKIND));
-  CUDA_TRY(h, cudaMemset(h->xmat, 0, sizeof(int64_t) * P2P_MAXW * P2P_MAXW));
-  CUDA_TRY(h, cudaMemset(h->flags, 0, sizeof(uint64_t) * P2P_NKIND * P2P_MAXW));
-  CUDA_TRY(h, cudaMemset(h->rt, 0, sizeof(RouteTable)));
-  constexpr int NB = 5;
-  void *mine[NB] = {h->xmat, h->flags, h->recv_keys, h->uniq_rows, h->grecv};
-  std::vector<cudaIpcMemHandle_t> hs(NB);
-  for (int b = 0; b < NB; ++b) CUDA_TRY(h, cudaIpcGetMemHandle(&hs[b], mine[b]));
-  const size_t bytes = sizeof(cudaIpcMemHandle_t) * NB;
+  RankInfo mine{};
+  mine.max_ids = h->max_ids;
+  {
+    char hn[256] = {0};
+    gethostname(hn, sizeof(hn) - 1);
+    uint64_t x = 1469598103934665603ull;  // FNV-1a of the host name
+    for (const char *c = hn; *c; ++c) x = (x ^ (unsigned char)*c) * 1099511628211ull;
+    mine.host = x;
+  }
+  CUDA_TRY(h, cudaDeviceGetPCIBusId(mine.busid, sizeof(mine.busid), h->device));
+  char *dsend = nullptr, *drecv = nullptr;
+  CUDA_TRY(h, cudaMalloc(&dsend, sizeof(RankInfo)));
+  CUDA_TRY(h, cudaMalloc(&drecv, sizeof(RankInfo) * W));
+  CUDA_TRY(h, cudaMemcpy(dsend, &mine, sizeof(RankInfo), cudaMemcpyHostToDevice));
+  NCCL_TRY(h, ncclAllGather(dsend, drecv, sizeof(RankInfo), ncclUint8, h->comm, 0));
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  std::vector<RankInfo> all(W);
+  CUDA_TRY(h, cudaMemcpy(all.data(), drecv, sizeof(RankInfo) * W, cudaMemcpyDeviceToHost));
+  cudaFree(dsend);
+  cudaFree(drecv);
+  int64_t cap = 0;
+  for (int r = 0; r < W; ++r) {
+    cap = std::max(cap, all[r].max_ids);
+    if (all[r].host != mine.host)
+      return fail(h, EMB_ERR_INVALID, "world > 1 needs every rank on one host (peer-memory exchange)");
+    if (r == h->rank) continue;
+    int dev = -1, ok = 0;
+    if (cudaDeviceGetByPCIBusId(&dev, all[r].busid) != cudaSuccess || dev < 0 ||
+        cudaDeviceCanAccessPeer(&ok, h->device, dev) != cudaSuccess || !ok)
+      return fail(h, EMB_ERR_INVALID,
+                  std::string("world > 1 needs peer access to every rank's GPU; no access to ") + all[r].busid);
+  }
+  *cap_out = cap;
+  return EMB_OK;
+}
+
+// multi-process: map every peer's exchange buffers and table shard (CUDA IPC handles all-gathered
+// over NCCL once)
+emb_status_t setup_ipc(emb_ctx *h) {
+  const int W = h->world;
+  void *mine[NB_PEER];
+  peer_buffers(h, mine);
+  std::vector<cudaIpcMemHandle_t> hs(NB_PEER);
+  for (int b = 0; b < NB_PEER; ++b) CUDA_TRY(h, cudaIpcGetMemHandle(&hs[b], mine[b]));
+  const size_t bytes = sizeof(cudaIpcMemHandle_t) * NB_PEER;
   char *dsend = nullptr, *drecv = nullptr;
   CUDA_TRY(h, cudaMalloc(&dsend, bytes));
   CUDA_TRY(h, cudaMalloc(&drecv, bytes * W));
   CUDA_TRY(h, cudaMemcpy(dsend, hs.data(), bytes, cudaMemcpyHostToDevice));
   NCCL_TRY(h, ncclAllGather(dsend, drecv, bytes, ncclUint8, h->comm, 0));
   CUDA_TRY(h, cudaDeviceSynchronize());
-  std::vector<cudaIpcMemHandle_t> all((size_t)NB * W);
+  std::vector<cudaIpcMemHandle_t> all((size_t)NB_PEER * W);
   CUDA_TRY(h, cudaMemcpy(all.data(), drecv, bytes * W, cudaMemcpyDeviceToHost));
   cudaFree(dsend);
   cudaFree(drecv);
-  P2PArgs &p = h->p2p;
-  p.world = W;
-  p.rank = h->rank;
-  p.flags = h->flags;
-  p.xmat = h->xmat;
-  p.rt = h->rt;
-  p.done = h->p2p_done;
+  init_p2p_args(h);
   for (int r = 0; r < W; ++r) {
-    void *ptr[NB];
-    for (int b = 0; b < NB; ++b) {
+    void *ptr[NB_PEER];
+    for (int b = 0; b < NB_PEER; ++b) {
       if (r == h->rank) {
         ptr[b] = mine[b];
       } else {
         void *q = nullptr;
-        CUDA_TRY(h, cudaIpcOpenMemHandle(&q, all[(size_t)r * NB + b], cudaIpcMemLazyEnablePeerAccess));
+        CUDA_TRY(h, cudaIpcOpenMemHandle(&q, all[(size_t)r * NB_PEER + b], cudaIpcMemLazyEnablePeerAccess));
         h->ipc_opened.push_back(q);
         ptr[b] = q;
       }
     }
-    p.peer_xmat[r] = static_cast<int64_t *>(ptr[0]);
-    p.peer_flags[r] = static_cast<uint64_t *>(ptr[1]);
-    p.peer_recv_keys[r] = static_cast<uint32_t *>(ptr[2]);
-    p.peer_uniq_rows[r] = static_cast<float *>(ptr[3]);
-    p.peer_grecv[r] = static_cast<float *>(ptr[4]);
+    set_peer(h, r, ptr);
   }
   return EMB_OK;
 }
 
-// p2p mode: bring the step's counts (device route table) to the host, for statistics only
+// group mode: every rank is a handle of this process; peers' buffers are plain pointers (peer access
+// enabled between distinct devices)
+emb_status_t setup_group(std::vector<emb_ctx *> &hs) {
+  const int W = (int)hs.size();
+  for (int r = 0; r < W; ++r) {
+    emb_ctx *h = hs[r];
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    for (int p = 0; p < W; ++p) {
+      if (hs[p]->device == h->device) continue;
+      int ok = 0;
+      CUDA_TRY(h, cudaDeviceCanAccessPeer(&ok, h->device, hs[p]->device));
+      if (!ok) return fail(h, EMB_ERR_INVALID, "emb_create_group: no peer access between the ranks' devices");
+      cudaError_t e = cudaDeviceEnablePeerAccess(hs[p]->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+    }
+    init_p2p_args(h);
+    for (int p = 0; p < W; ++p) {
+      void *ptr[NB_PEER];
+      peer_buffers(hs[p], ptr);
+      set_peer(h, p, ptr);
+    }
+  }
+  return EMB_OK;
+}
+
+// bring the last step's counts to the host (statistics only)
 emb_status_t sync_counts(emb_ctx *h) {
   if (h->counts_synced) return EMB_OK;
   if (h->last_stream) CUDA_TRY(h, cudaStreamSynchronize(h->last_stream));
-  RouteTable rt;
-  CUDA_TRY(h, cudaMemcpy(&rt, h->rt, sizeof(rt), cudaMemcpyDeviceToHost));
+  CUDA_TRY(h, cudaStreamSynchronize(h->side));
   const int W = h->world;
-  for (int p = 0; p <= W; ++p) {
-    h->soff[p] = rt.soff[p];
-    h->roff[p] = rt.roff[p];
-  }
+  int64_t sc[P2P_MAXW], xm[4 * P2P_MAXW], nm = 0;
+  CUDA_TRY(h, cudaMemcpy(sc, h->scnt, sizeof(int64_t) * P2P_MAXW, cudaMemcpyDeviceToHost));
+  CUDA_TRY(h, cudaMemcpy(xm, h->xmat, sizeof(int64_t) * 4 * P2P_MAXW, cudaMemcpyDeviceToHost));
+  CUDA_TRY(h, cudaMemcpy(&nm, h->n_merged, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  int64_t ul = 0;
   for (int p = 0; p < W; ++p) {
-    h->send_counts[p] = rt.soff[p + 1] - rt.soff[p];
-    h->recv_counts[p] = rt.recv_counts[p];
+    h->send_counts[p] = sc[p];
+    h->recv_counts[p] = xm[xmat_idx(h->epoch, 0, p)];
+    ul += sc[p];
   }
-  h->U_l = rt.n_send;
-  h->n_recv = rt.n_recv;
+  h->U_l = ul;
+  h->n_recv = nm;
   h->counts_synced = true;
   return EMB_OK;
 }
 
-emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
+// group_cap > 0: group mode (every rank in this process; the caller computed the region size)
+emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap) {
   if (!cfg) return fail(h, EMB_ERR_INVALID, "cfg is NULL");
   if (cfg->num_tables < 1 || cfg->num_tables > EMB_MAX_TABLES || !cfg->rows)
     return fail(h, EMB_ERR_INVALID, "num_tables must be in [1, EMB_MAX_TABLES] and rows non-NULL");
@@ -331,7 +418,8 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
     return fail(h, EMB_ERR_INVALID, "max_batch >= 1 and 1 <= max_ids < 2^30 required");
   if (cfg->world < 1 || cfg->world > EMB_MAX_WORLD || cfg->rank < 0 || cfg->rank >= cfg->world)
     return fail(h, EMB_ERR_INVALID, "need 1 <= world <= EMB_MAX_WORLD and 0 <= rank < world");
-  if (cfg->world > 1 && !cfg->nccl_id) return fail(h, EMB_ERR_INVALID, "world > 1 needs nccl_id");
+  if (cfg->world > 1 && !group_cap && !cfg->nccl_id)
+    return fail(h, EMB_ERR_INVALID, "world > 1 needs nccl_id (or emb_create_group)");
   if (cfg->shard != EMB_SHARD_CYCLIC && cfg->shard != EMB_SHARD_BLOCK) return fail(h, EMB_ERR_INVALID, "bad shard");
   if ((int64_t)cfg->num_slots * cfg->max_batch >= (1ll << 31))
     return fail(h, EMB_ERR_INVALID, "num_slots * max_batch must be < 2^31");
@@ -363,40 +451,39 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   h->world = cfg->world;
   h->device = cfg->device;
   h->shard = cfg->shard;
+  h->group = group_cap > 0;
 
-  // key space
+  // key space: sorted keys are the fused rows g at every W
   KeySpace &ks = h->ks;
   ks.world = h->world;
   ks.rank = h->rank;
   ks.shard = h->shard;
-  ks.rows_per = (h->R_total + h->world - 1) / h->world;
+  ks.rows_per = (uint32_t)((h->R_total + h->world - 1) / h->world);
+  ks.key_bits = std::max<uint32_t>(1, bits_for(h->R_total));  // max valid key R-1 < sentinel-mask 2^b - 1
   if (h->world == 1) {
-    h->rows_local = h->rows_local_max = (int64_t)h->R_total;
-    ks.lbits = 32;
-    ks.key_bits = bits_for(h->R_total);  // max valid key R-1 < sentinel-mask 2^b - 1
-    if (ks.key_bits == 0) ks.key_bits = 1;
-    h->lmask = 0xFFFFFFFFu;
+    h->rows_local = (int64_t)h->R_total;
+  } else if (h->shard == 0) {
+    h->rows_local = (int64_t)((h->R_total - h->rank + h->world - 1) / h->world);
   } else {
-    const uint64_t W = h->world;
-    if (h->shard == 0) {
-      h->rows_local = (int64_t)((h->R_total - h->rank + W - 1) / W);
-      h->rows_local_max = (int64_t)((h->R_total + W - 1) / W);
-    } else {
-      const int64_t lo = std::min<int64_t>((int64_t)h->R_total, (int64_t)ks.rows_per * h->rank);
-      const int64_t hi = std::min<int64_t>((int64_t)h->R_total, (int64_t)ks.rows_per * (h->rank + 1));
-      h->rows_local = hi - lo;
-      h->rows_local_max = (int64_t)ks.rows_per;
-    }
-    ks.lbits = bits_for((uint64_t)h->rows_local_max - 1);
-    if (ks.lbits == 0) ks.lbits = 1;
-    const uint64_t max_valid = ((uint64_t)(h->world - 1) << ks.lbits) + (uint64_t)h->rows_local_max - 1;
-    if (max_valid + 1 >= 0xFFFFFFFFull) return fail(h, EMB_ERR_INVALID, "routing key space exceeds 32 bits");
-    ks.key_bits = bits_for(max_valid + 1);
-    h->lmask = (1u << ks.lbits) - 1u;
-    h->owner_key_bits = ks.lbits;
+    const int64_t lo = std::min<int64_t>((int64_t)h->R_total, (int64_t)ks.rows_per * h->rank);
+    const int64_t hi = std::min<int64_t>((int64_t)h->R_total, (int64_t)ks.rows_per * (h->rank + 1));
+    h->rows_local = hi - lo;
   }
 
   CUDA_TRY(h, cudaSetDevice(h->device));
+  const int W = h->world;
+  if (W > 1 && !h->group) {
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_id, sizeof(id));
+    NCCL_TRY(h, ncclCommInitRank(&h->comm, W, id, h->rank));
+    emb_status_t hs = mp_handshake(h, &h->cap);
+    if (hs != EMB_OK) return hs;
+  } else if (W > 1) {
+    h->cap = group_cap;
+  }
+  if (W > 1 && (int64_t)W * h->cap >= (1ll << 31) - 1)
+    return fail(h, EMB_ERR_INVALID, "world * max_ids must be < 2^31 - 1");
+
   // table shard + state
   const size_t row_elems = (size_t)std::max<int64_t>(h->rows_local, 1) * h->D;
   if (dalloc(h, &h->w, row_elems) != cudaSuccess) return fail(h, EMB_ERR_NOMEM, "cannot allocate the table shard");
@@ -405,8 +492,8 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   if (h->opt == EMB_OPT_ROWWISE_ADAGRAD && dalloc(h, &h->a, (size_t)std::max<int64_t>(h->rows_local, 1)) != cudaSuccess)
     return fail(h, EMB_ERR_NOMEM, "cannot allocate the row-wise Adagrad state");
   {
-    // the side stream carries the latency-critical sort: highest priority, so its CTAs are scheduled
-    // ahead of the bandwidth-bound pool CTAs as SMs free up
+    // the side stream carries the latency-critical sort (W = 1) / owner merge (W > 1): highest
+    // priority, so its CTAs are scheduled ahead of the bandwidth-bound pool CTAs as SMs free up
     int lo_prio = 0, hi_prio = 0;
     CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     CUDA_TRY(h, cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi_prio));
@@ -414,6 +501,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_pf, cudaEventDisableTiming));
+  CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_phase, cudaEventDisableTiming));
   CUDA_TRY(h, launch_init(h->w, h->a, h->opt == EMB_OPT_ROWWISE_ADAGRAD, h->rows_local, h->D, h->seed,
                           h->init_accum, ks, h->rank, h->side));
 
@@ -426,62 +514,62 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
 
   // workspace
   const int64_t N = h->max_ids, SB = (int64_t)h->S * h->max_batch;
-  const int W = h->world;
-  h->recv_cap = W > 1 ? (int64_t)W * N : N;
-  const int64_t grad_n = std::max<int64_t>(N, h->recv_cap);
-  const int64_t nticket = grad_n + 1;
+  const int64_t WC = W > 1 ? (int64_t)W * h->cap : 0;
+  h->nticket = std::max<int64_t>(N, WC) + 1;
   const int64_t nwarps_max = grad_max_warps(h->device);
   bool bad = false;
   bad |= dalloc(h, &h->key_csr, N) != cudaSuccess;
   bad |= dalloc(h, &h->drow, N) != cudaSuccess;
   bad |= dalloc(h, &h->k0, N) != cudaSuccess;
   bad |= dalloc(h, &h->v0, N) != cudaSuccess;
-  if (h->world == 1) {
+  bad |= dalloc(h, &h->sort_scratch, N) != cudaSuccess;
+  if (W == 1) {
     bad |= dalloc(h, &h->sk_set[1], N) != cudaSuccess;
     bad |= dalloc(h, &h->sp_set[1], N) != cudaSuccess;
-    bad |= dalloc(h, &h->sort_scratch, N) != cudaSuccess;
   }
   bad |= dalloc(h, &h->k1, N) != cudaSuccess;
   bad |= dalloc(h, &h->v1, N) != cudaSuccess;
   bad |= dalloc(h, &h->blen, SB) != cudaSuccess;
-  const int64_t sort_n = std::max<int64_t>(N, h->recv_cap);
   uint32_t *sort_words = nullptr;
-  const size_t sww = sort_workspace_words(sort_n);
-  bad |= dalloc(h, &sort_words, sww) != cudaSuccess;
+  bad |= dalloc(h, &sort_words, sort_workspace_words(N)) != cudaSuccess;
   bad |= dalloc(h, &h->partials, (size_t)2 * nwarps_max * h->D) != cudaSuccess;
-  bad |= dalloc(h, &h->tickets, nticket) != cudaSuccess;
-  bad |= dalloc(h, &h->useg, sort_n) != cudaSuccess;
-  bad |= dalloc(h, &h->ukey, sort_n) != cudaSuccess;
-  bad |= dalloc(h, &h->ustart, sort_n + 1) != cudaSuccess;
-  bad |= dalloc(h, &h->uend, sort_n + 1) != cudaSuccess;
+  bad |= dalloc(h, &h->tickets, h->nticket) != cudaSuccess;
+  bad |= dalloc(h, &h->useg, N) != cudaSuccess;
+  bad |= dalloc(h, &h->ukey, N) != cudaSuccess;
+  bad |= dalloc(h, &h->ustart, N + 1) != cudaSuccess;
+  bad |= dalloc(h, &h->uend, N + 1) != cudaSuccess;
   bad |= dalloc(h, &h->u_count, 2) != cudaSuccess;
-  bad |= dalloc(h, &h->uniq_status, unique_status_words(sort_n)) != cudaSuccess;
+  bad |= dalloc(h, &h->uniq_status, unique_status_words(N)) != cudaSuccess;
   bad |= dalloc(h, &h->uniq_counter, 1) != cudaSuccess;
   bad |= dalloc(h, &h->fin, 3) != cudaSuccess;
   bad |= dalloc(h, &h->err_dev, 1) != cudaSuccess;
   if (W > 1) {
     bad |= dalloc(h, &h->inv, N) != cudaSuccess;
-    bad |= dalloc(h, &h->send_keys, N) != cudaSuccess;
-    bad |= dalloc(h, &h->recv_keys, h->recv_cap) != cudaSuccess;
-    bad |= dalloc(h, &h->owner_rows, (size_t)h->recv_cap * h->D) != cudaSuccess;
-    bad |= dalloc(h, &h->uniq_rows, (size_t)N * h->D) != cudaSuccess;
-    bad |= dalloc(h, &h->gloc, (size_t)N * h->D) != cudaSuccess;
-    bad |= dalloc(h, &h->grecv, (size_t)h->recv_cap * h->D) != cudaSuccess;
-    bad |= dalloc(h, &h->ok0, h->recv_cap) != cudaSuccess;
-    bad |= dalloc(h, &h->ov0, h->recv_cap) != cudaSuccess;
-    bad |= dalloc(h, &h->ok1, h->recv_cap) != cudaSuccess;
-    bad |= dalloc(h, &h->ov1, h->recv_cap) != cudaSuccess;
-    bad |= dalloc(h, &h->d_counts, 2 * EMB_MAX_WORLD) != cudaSuccess;
-    bad |= dalloc(h, &h->ouseg, h->recv_cap) != cudaSuccess;
-    bad |= dalloc(h, &h->oukey, h->recv_cap) != cudaSuccess;
-    bad |= dalloc(h, &h->oustart, h->recv_cap + 1) != cudaSuccess;
-    bad |= dalloc(h, &h->ouend, h->recv_cap + 1) != cudaSuccess;
-    bad |= dalloc(h, &h->ou_count, 2) != cudaSuccess;
-    bad |= dalloc(h, &h->ouniq_status, unique_status_words(h->recv_cap)) != cudaSuccess;
-    bad |= dalloc(h, &h->ouniq_counter, 1) != cudaSuccess;
-    bad |= dalloc(h, &h->sp, N) != cudaSuccess;
     bad |= dalloc(h, &h->outidx, N) != cudaSuccess;
-    bad |= dalloc(h, &h->tcnt, (size_t)((N + 2047) / 2048 + 1) * EMB_MAX_WORLD) != cudaSuccess;
+    bad |= dalloc(h, &h->send_local, WC) != cudaSuccess;
+    bad |= dalloc(h, &h->scnt, P2P_MAXW) != cudaSuccess;
+    bad |= dalloc(h, &h->route_tot, P2P_MAXW) != cudaSuccess;
+    bad |= dalloc(h, &h->route_counter, 1) != cudaSuccess;
+    bad |= dalloc(h, &h->route_done, 1) != cudaSuccess;
+    bad |= dalloc(h, &h->route_status, route_status_words(N)) != cudaSuccess;
+    bad |= dalloc(h, &h->recv_keys, 2 * WC) != cudaSuccess;
+    bad |= dalloc(h, &h->uniq_rows, (size_t)WC * h->D) != cudaSuccess;
+    bad |= dalloc(h, &h->grecv, (size_t)2 * WC * h->D) != cudaSuccess;  // hi and lo parts
+    bad |= dalloc(h, &h->ok0, WC) != cudaSuccess;
+    bad |= dalloc(h, &h->ov0, WC) != cudaSuccess;
+    bad |= dalloc(h, &h->ok1, WC) != cudaSuccess;
+    bad |= dalloc(h, &h->ov1, WC) != cudaSuccess;
+    bad |= dalloc(h, &h->n_merged, 1) != cudaSuccess;
+    bad |= dalloc(h, &h->xmat, 4 * P2P_MAXW) != cudaSuccess;
+    bad |= dalloc(h, &h->flags, (size_t)P2P_NKIND * P2P_MAXW) != cudaSuccess;
+    bad |= dalloc(h, &h->p2p_done, P2P_NKIND) != cudaSuccess;
+    bad |= dalloc(h, &h->ouseg, WC) != cudaSuccess;
+    bad |= dalloc(h, &h->oukey, WC) != cudaSuccess;
+    bad |= dalloc(h, &h->oustart, WC + 1) != cudaSuccess;
+    bad |= dalloc(h, &h->ouend, WC + 1) != cudaSuccess;
+    bad |= dalloc(h, &h->ou_count, 2) != cudaSuccess;
+    bad |= dalloc(h, &h->ouniq_status, unique_status_words(WC)) != cudaSuccess;
+    bad |= dalloc(h, &h->ouniq_counter, 1) != cudaSuccess;
   }
   if (bad) return fail(h, EMB_ERR_NOMEM, "cannot allocate the step workspace");
   h->sk_set[0] = h->k0;
@@ -489,10 +577,10 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   h->sws.hist = sort_words;
   h->sws.counters = sort_words + 4 * 256;
   h->sws.status = sort_words + 4 * 256 + 4;
-  h->sws.max_tiles = (sort_n + 4095) / 4096 + 1;
+  h->sws.max_tiles = (N + 4095) / 4096 + 1;
   h->sws.err = h->err_dev;
-  CUDA_TRY(h, cudaMemset(h->tickets, 0, sizeof(uint32_t) * nticket));
-  // table groups of the slot-major CSR (segsort fast path needs a non-decreasing slot_table)
+  CUDA_TRY(h, cudaMemset(h->tickets, 0, sizeof(uint32_t) * h->nticket));
+  // table groups of the slot-major CSR (the per-table sort needs a non-decreasing slot_table)
   {
     h->segsort_ok = true;
     for (int s = 1; s < h->S; ++s)
@@ -513,8 +601,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
       gslot.push_back(h->S);
       h->G = (int32_t)gbase.size();
       // key ranges (CTAs) per group: ~4K occurrences per CTA at the capacity bound (K sweep on C2:
-      // K=2/4/8/16 -> 206/157/176/201 us per step); every CTA scans
-      // its whole group, so K stays small
+      // K=2/4/8/16 -> 206/157/176/201 us per step); every CTA scans its whole group, so K stays small
       const int64_t per = (h->max_ids + h->G - 1) / h->G;
       h->segK = (int32_t)std::min<int64_t>(16, std::max<int64_t>(1, (per + 4095) / 4096));
       if (const char *ek = getenv("EMB_SEGK")) h->segK = std::max(1, std::min(32, atoi(ek)));  // experiment knob
@@ -532,35 +619,33 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h) {
   CUDA_TRY(h, cudaMemset(h->err_dev, 0, sizeof(uint32_t)));
   CUDA_TRY(h, cudaMemset(h->fin, 0, 3 * sizeof(uint32_t)));
   CUDA_TRY(h, cudaMemset(h->uniq_counter, 0, sizeof(uint32_t)));
-  CUDA_TRY(h, cudaMemset(h->uniq_status, 0, sizeof(uint64_t) * unique_status_words(sort_n)));
-  if (h->ouniq_status) {
-    CUDA_TRY(h, cudaMemset(h->ouniq_counter, 0, sizeof(uint32_t)));
-    CUDA_TRY(h, cudaMemset(h->ouniq_status, 0, sizeof(uint64_t) * unique_status_words(h->recv_cap)));
-  }
+  CUDA_TRY(h, cudaMemset(h->uniq_status, 0, sizeof(uint64_t) * unique_status_words(N)));
   CUDA_TRY(h, cudaMemset(h->u_count, 0, 2 * sizeof(uint32_t)));
+  if (W > 1) {
+    CUDA_TRY(h, cudaMemset(h->ouniq_counter, 0, sizeof(uint32_t)));
+    CUDA_TRY(h, cudaMemset(h->ouniq_status, 0, sizeof(uint64_t) * unique_status_words(WC)));
+    CUDA_TRY(h, cudaMemset(h->route_tot, 0, sizeof(uint32_t) * P2P_MAXW));
+    CUDA_TRY(h, cudaMemset(h->route_counter, 0, sizeof(uint32_t)));
+    CUDA_TRY(h, cudaMemset(h->route_done, 0, sizeof(uint32_t)));
+    CUDA_TRY(h, cudaMemset(h->route_status, 0, sizeof(uint64_t) * route_status_words(N)));
+    CUDA_TRY(h, cudaMemset(h->scnt, 0, sizeof(int64_t) * P2P_MAXW));
+    CUDA_TRY(h, cudaMemset(h->n_merged, 0, sizeof(int64_t)));
+    CUDA_TRY(h, cudaMemset(h->xmat, 0, sizeof(int64_t) * 4 * P2P_MAXW));
+    CUDA_TRY(h, cudaMemset(h->flags, 0, sizeof(uint64_t) * P2P_NKIND * P2P_MAXW));
+    CUDA_TRY(h, cudaMemset(h->p2p_done, 0, sizeof(uint32_t) * P2P_NKIND));
+  }
   void *hp = nullptr;
   if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) != cudaSuccess)
     return fail(h, EMB_ERR_NOMEM, "cannot allocate pinned error word");
   h->err_host = static_cast<uint32_t *>(hp);
   *h->err_host = 0;
   CUDA_TRY(h, cudaHostGetDevicePointer(reinterpret_cast<void **>(&h->err_host_dev), hp, 0));
-  if (W > 1) {
-    void *hc = nullptr;
-    if (cudaHostAlloc(&hc, sizeof(int64_t) * (2 * EMB_MAX_WORLD + 2), cudaHostAllocDefault) != cudaSuccess)
-      return fail(h, EMB_ERR_NOMEM, "cannot allocate pinned counts");
-    h->h_counts = static_cast<int64_t *>(hc);
-    ncclUniqueId id;
-    std::memcpy(&id, cfg->nccl_id, sizeof(id));
-    NCCL_TRY(h, ncclCommInitRank(&h->comm, W, id, h->rank));
-    const char *ex = getenv("EMB_EXCHANGE");  // "nccl" selects the v1 grouped send/recv exchange
-    h->use_p2p = h->segsort_ok && !(ex && std::strcmp(ex, "nccl") == 0);
-    if (h->use_p2p) {
-      emb_status_t ps = setup_p2p(h);
-      if (ps != EMB_OK) return ps;
-    }
-  }
   CUDA_TRY(h, cudaStreamSynchronize(h->side));
   CUDA_TRY(h, cudaDeviceSynchronize());
+  if (W > 1 && !h->group) {
+    emb_status_t ps = setup_ipc(h);
+    if (ps != EMB_OK) return ps;
+  }
   return EMB_OK;
 }
 
@@ -572,12 +657,12 @@ void destroy_impl(emb_ctx *h) {
   if (h->comm) ncclCommDestroy(h->comm);
   for (void *p : h->allocs) cudaFree(p);
   if (h->err_host) cudaFreeHost(h->err_host);
-  if (h->h_counts) cudaFreeHost(h->h_counts);
   for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
-  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
-  if (h->ev_join) cudaEventDestroy(h->ev_join);
-  if (h->ev_pf) cudaEventDestroy(h->ev_pf);
+  for (cudaEvent_t e : {h->ev_fork, h->ev_join, h->ev_pf, h->ev_phase, h->ev_h2d[0], h->ev_h2d[1], h->ev_d2h[0],
+                        h->ev_d2h[1]})
+    if (e) cudaEventDestroy(e);
   if (h->side) cudaStreamDestroy(h->side);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   delete h;
 }
 
@@ -592,26 +677,7 @@ void destroy_impl(emb_ctx *h) {
     ++h->launches;                                                 \
   } while (0)
 
-emb_status_t exchange(emb_ctx *h, const void *sendbuf, const int64_t *scnt, const int64_t *soff, void *recvbuf,
-                      const int64_t *rcnt, const int64_t *roff, size_t elem_bytes, ncclDataType_t dt,
-                      int64_t elems_per_item, cudaStream_t st) {
-  prof_hook(h, KID_NCCL, 0, st);
-  NCCL_TRY(h, ncclGroupStart());
-  for (int p = 0; p < h->world; ++p) {
-    if (scnt[p] > 0)
-      NCCL_TRY(h, ncclSend(static_cast<const char *>(sendbuf) + (size_t)soff[p] * elems_per_item * elem_bytes,
-                           (size_t)scnt[p] * elems_per_item, dt, p, h->comm, st));
-    if (rcnt[p] > 0)
-      NCCL_TRY(h, ncclRecv(static_cast<char *>(recvbuf) + (size_t)roff[p] * elems_per_item * elem_bytes,
-                           (size_t)rcnt[p] * elems_per_item, dt, p, h->comm, st));
-  }
-  NCCL_TRY(h, ncclGroupEnd());
-  prof_hook(h, KID_NCCL, 1, st);
-  ++h->launches;
-  return EMB_OK;
-}
-
-// per-table sort arguments (W = 1 path) writing sort-output set `set`
+// per-table sort arguments writing sort-output set `set`
 SegSortArgs segsort_args(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz, int set) {
   SegSortArgs sa{};
   sa.ids = ids;
@@ -619,6 +685,7 @@ SegSortArgs segsort_args(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   sa.nnz = nnz;
   sa.batch = batch;
   sa.gslot = h->d_gslot;
+  sa.ngroups = h->G;
   sa.gbase = h->d_gbase;
   sa.grows = h->d_grows;
   sa.gbits = h->d_gbits;
@@ -661,24 +728,18 @@ emb_status_t lookup_prefetch_impl(emb_ctx *h, const int64_t *ids, const int64_t 
   return EMB_OK;
 }
 
-emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz,
-                         float *out, cudaStream_t st) {
-  if (h->state != 0) return fail(h, EMB_ERR_STATE, "emb_lookup called twice without emb_backward_update");
-  if (batch < 0 || batch > h->max_batch) return fail(h, EMB_ERR_INVALID, "batch out of [0, max_batch]");
-  if (nnz < 0 || nnz > h->max_ids) return fail(h, EMB_ERR_INVALID, "nnz out of [0, max_ids]");
-  if (batch == 0 && nnz != 0) return fail(h, EMB_ERR_INVALID, "nnz must be 0 when batch == 0");
-  if ((batch > 0 && (!offsets || !out)) || (nnz > 0 && !ids))
-    return fail(h, EMB_ERR_INVALID, "NULL ids/offsets/out");
-  if (batch > 0 && !aligned16(out)) return fail(h, EMB_ERR_INVALID, "out must be 16-byte aligned");
-  emb_status_t s = check_sticky(h);
-  if (s != EMB_OK) return s;
-  CUDA_TRY(h, cudaSetDevice(h->device));
-  h->launches = 0;
-  h->batch = batch;
-  h->nnz = nnz;
-  h->last_stream = st;
-  const bool mean = h->pool == EMB_POOL_MEAN;
+// argument checks shared by every lookup entry point ("" = fine)
+const char *lookup_arg_error(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz,
+                             const float *out) {
+  if (batch < 0 || batch > h->max_batch) return "batch out of [0, max_batch]";
+  if (nnz < 0 || nnz > h->max_ids) return "nnz out of [0, max_ids]";
+  if (batch == 0 && nnz != 0) return "nnz must be 0 when batch == 0";
+  if ((batch > 0 && (!offsets || !out)) || (nnz > 0 && !ids)) return "NULL ids/offsets/out";
+  if (batch > 0 && !aligned16(out)) return "out must be 16-byte aligned";
+  return "";
+}
 
+KeysArgs keys_args(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz) {
   KeysArgs ka{};
   ka.ids = ids;
   ka.offsets = offsets;
@@ -688,16 +749,15 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   ka.slot_table = h->d_slot_table;
   ka.base = h->d_base;
   ka.rows = h->d_rows;
-  ka.ks = h->ks;
   ka.key = h->key_csr;
   ka.drow = h->drow;
   ka.blen = h->blen;
   ka.err = h->err_dev;
-  // with the per-table sort, the pool and the sort read the ids themselves (no key kernel); at W > 1
-  // the pool then takes each occurrence's received row through row_idx
-  const bool direct = h->segsort_ok;
-  if (batch > 0 && !direct) LAUNCH(h, KID_KEYS, st, launch_keys(ka, st));
+  return ka;
+}
 
+PoolArgs pool_args(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz, float *out) {
+  const bool mean = h->pool == EMB_POOL_MEAN;
   PoolArgs pa{};
   pa.key = h->key_csr;
   pa.offsets = offsets;
@@ -709,7 +769,13 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   pa.out = out;
   pa.err = h->err_dev;
   pa.err_host = h->err_host_dev;
-  if (direct) {
+  pa.ks = h->ks;
+  pa.rows_src = h->w;
+  pa.nrows_src = h->rows_local;
+  pa.rows_remote = h->uniq_rows;
+  pa.nrows_remote = h->world > 1 ? (int64_t)h->world * h->cap : 0;
+  pa.row_idx = h->inv;
+  if (h->segsort_ok) {  // direct mode: the pool reads the ids itself (no key kernel)
     pa.ids = ids;
     pa.slot_table = h->d_slot_table;
     pa.base = h->d_base;
@@ -717,211 +783,134 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
     pa.drow = h->drow;
     pa.blen = mean ? h->blen : nullptr;
   }
+  return pa;
+}
 
-  if (h->world == 1) {
-    // fork: the sort runs on the side stream while the pool streams rows on the caller stream
-    CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
-    CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-    // a sort prefetched for exactly these inputs (emb_lookup_prefetch) is already queued on the side
-    // stream: consume it (the join below waits for it)
-    const bool use_pf = h->pf.valid && h->pf.ids == ids && h->pf.offsets == offsets && h->pf.batch == batch &&
-                        h->pf.nnz == nnz;
-    h->pf.valid = false;
-    if (use_pf) {
-      h->cur_set = h->pf.set;
-      h->skey = h->sk_set[h->cur_set];
-      h->spay = h->sp_set[h->cur_set];
-    } else if (h->segsort_ok) {
-      h->cur_set ^= 1;  // (stream-ordered after the previous backward: either set is free)
-      SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, h->cur_set);
-      sa.fin = (batch > 0 && nnz > 0) ? h->fin : nullptr;  // the later of sort / pool publishes the error word
-      h->skey = sa.skey;
-      h->spay = sa.spay;
-      static int serial = -1;  // experiment knob: EMB_SERIAL=1 runs the sort before the pool (no overlap)
-      if (serial < 0) serial = getenv("EMB_SERIAL") ? atoi(getenv("EMB_SERIAL")) : 0;
-      cudaStream_t ss = serial ? st : h->side;
-      if (batch > 0) LAUNCH(h, KID_SORT_PASS, ss, launch_segsort(sa, h->G, ss));
-    } else {
-      int nl = 0;
-      cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz,
-                                       h->ks.key_bits, h->side, &h->skey, &h->spay, &nl, prof_hook, h);
-      if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
-      h->launches += nl;
-    }
-    pa.rows_src = h->w;
-    pa.nrows_src = h->rows_local;
-    pa.row_idx = nullptr;
-    const bool fused_pub = h->segsort_ok && batch > 0 && nnz > 0;
-    pa.fin = fused_pub ? h->fin : nullptr;
-    pa.fin_kernels = use_pf ? 1 : 2;  // a prefetched sort does not take part in the publish
-    if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
-    CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
-    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
-    if (batch > 0 && !fused_pub) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
-    h->U_l = -1;  // computed on demand
-    h->state = 1;
-    return EMB_OK;
-  }
-
-  // ---------------- world > 1
-  const int W = h->world;
-  int nl = 0;
-  cudaError_t e = cudaSuccess;
-  if (h->segsort_ok) {
-    // per-table sort by fused key g, dedup, then a stable partition of the distinct keys by owner
-    SegSortArgs sa{};
-    sa.ids = ids;
-    sa.offsets = offsets;
-    sa.nnz = nnz;
-    sa.batch = batch;
-    sa.gslot = h->d_gslot;
-    sa.gbase = h->d_gbase;
-    sa.grows = h->d_grows;
-    sa.gbits = h->d_gbits;
-    sa.skey = h->k0;
-    sa.spay = h->v0;
-    sa.scratch_k = h->k1;
-    sa.scratch_a = h->v1;
-    sa.scratch_b = h->outidx;  // overwritten later in this step
-    sa.run_k = h->run_k;
-    sa.run_i = h->run_i;
-    sa.K = h->segK;
-    sa.err = h->err_dev;
-    h->skey = h->k0;
-    h->spay = h->v0;
-    if (batch > 0) LAUNCH(h, KID_SORT_PASS, st, launch_segsort(sa, h->G, st));
-    UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter, ++h->uniq_epoch};
-    LAUNCH(h, KID_UNIQUE, st, launch_unique(ua, st));
-    LAUNCH(h, KID_ROUTE, st,
-           launch_partition(h->ukey, h->u_count, nnz, h->ks, h->tcnt, h->send_keys, h->sp, h->d_counts, st));
-    LAUNCH(h, KID_ROUTE, st, launch_outidx(h->skey, h->spay, h->useg, h->sp, nnz, h->outidx, h->inv, st));
-    h->ukey_is_g = true;
-  } else {
-    e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz, h->ks.key_bits, st,
-                         &h->skey, &h->spay, &nl, prof_hook, h);
-    if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
-    h->launches += nl;
-    UniqueArgs ua{h->skey, nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter, ++h->uniq_epoch};
-    LAUNCH(h, KID_UNIQUE, st, launch_unique(ua, st));
-    LAUNCH(h, KID_ROUTE, st, launch_owner_counts(h->ukey, h->u_count, W, h->ks.lbits, h->d_counts, st));
-    LAUNCH(h, KID_ROUTE, st, launch_scatter_inverse(h->skey, h->spay, h->useg, nnz, h->inv, st));
-    LAUNCH(h, KID_ROUTE, st, launch_local_of_unique(h->ukey, h->u_count, nnz, h->lmask, h->send_keys, st));
-    h->ukey_is_g = false;
-  }
-  if (h->use_p2p) {
-    // ---- peer-memory exchange: no host synchronisation
-    P2PArgs px = h->p2p;
-    px.epoch = ++h->epoch;
-    const int64_t cap = h->recv_cap;
-    // X0 (counts + wait + route table), X1 (keys; its last block raises KEYS)
-    LAUNCH(h, KID_NCCL, st, launch_xcounts(px, h->d_counts, h->err_dev, st));
-    LAUNCH(h, KID_ROUTE, st, launch_push_keys(px, h->send_keys, nnz, st));
-    // consumers wait in a one-thread kernel, not in their own prologue: a spinning grid would hold
-    // SMs the concurrent side-stream merge and the gather need (measured slower at W = 4)
-    LAUNCH(h, KID_WAIT, st, launch_wait(px, P2P_KEYS, h->err_dev, st));
-    // owner side: stable W-way merge of the received runs, overlapped with the gather-push
-    CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
-    CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-    h->okey = h->ok0;
-    h->opay = h->ov0;
-    const bool fused_pub = batch > 0 && direct;  // the later of merge / pool publishes the error word
-    LAUNCH(h, KID_MERGE, h->side,
-           launch_merge_tree(h->recv_keys, h->rt->recv_counts, W, cap, h->ok0, h->ov0, h->ok1, h->ov1, h->err_dev,
-                             h->side, fused_pub ? h->fin : nullptr, h->err_host_dev));
-    // X2 fused with the gather (its last block raises ROWS)
-    LAUNCH(h, KID_OWNER_GATHER, st,
-           launch_gather_push(px, h->w, h->recv_keys, h->D, cap, h->rows_local, h->err_dev, st));
-    LAUNCH(h, KID_WAIT, st, launch_wait(px, P2P_ROWS, h->err_dev, st));
-    pa.rows_src = h->uniq_rows;
-    pa.nrows_src = h->max_ids;
-    pa.row_idx = h->inv;
-    pa.fin = fused_pub ? h->fin : nullptr;
-    pa.fin_kernels = 2;
-    if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
-    CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
-    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
-    if (batch > 0 && !fused_pub) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
-    h->counts_synced = false;
-    h->U_l = -1;
-    h->n_recv = -1;
-    h->owner_unique_done = false;
-    h->state = 1;
-    return EMB_OK;
-  }
-  // X0: per-peer counts
-  {
-    int64_t ones[EMB_MAX_WORLD], offs[EMB_MAX_WORLD];
-    for (int p = 0; p < W; ++p) {
-      ones[p] = 1;
-      offs[p] = p;
-    }
-    emb_status_t es = exchange(h, h->d_counts, ones, offs, h->d_counts + EMB_MAX_WORLD, ones, offs, sizeof(int64_t),
-                               ncclInt64, 1, st);
-    if (es != EMB_OK) return es;
-  }
-  CUDA_TRY(h, cudaMemcpyAsync(h->h_counts, h->d_counts, sizeof(int64_t) * 2 * EMB_MAX_WORLD, cudaMemcpyDeviceToHost,
-                              st));
-  CUDA_TRY(h, cudaStreamSynchronize(st));  // v1: the host sizes the all-to-allv from the counts
-  h->soff[0] = h->roff[0] = 0;
-  for (int p = 0; p < W; ++p) {
-    h->send_counts[p] = h->h_counts[p];
-    h->recv_counts[p] = h->h_counts[EMB_MAX_WORLD + p];
-    h->soff[p + 1] = h->soff[p] + h->send_counts[p];
-    h->roff[p + 1] = h->roff[p] + h->recv_counts[p];
-  }
-  h->U_l = h->soff[W];
-  h->n_recv = h->roff[W];
-  if (h->n_recv > h->recv_cap) return fail(h, EMB_ERR_INVALID, "received keys exceed the receive capacity");
-  // X1: local ids to their owners
-  emb_status_t es = exchange(h, h->send_keys, h->send_counts, h->soff, h->recv_keys, h->recv_counts, h->roff,
-                             sizeof(uint32_t), ncclUint32, 1, st);
-  if (es != EMB_OK) return es;
-  // owner side: the W received runs are each sorted by local id -> stable W-way merge (source-rank
-  // order inside a row) on the side stream, overlapped with the gather and X2
+emb_status_t lookup_w1(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz, float *out,
+                       cudaStream_t st) {
+  // key mode (general sort path): the key kernel feeds both the sort and the pool
+  if (batch > 0 && !h->segsort_ok) LAUNCH(h, KID_KEYS, st, launch_keys(keys_args(h, ids, offsets, batch, nnz), st));
+  // fork: the sort runs on the side stream while the pool streams rows on the caller stream
   CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
   CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-  if (h->ukey_is_g || h->shard == 1) {
-    h->okey = h->ok0;
-    h->opay = h->ov0;
-    LAUNCH(h, KID_SORT_PASS, h->side,
-           launch_merge_runs(h->recv_keys, h->d_counts + EMB_MAX_WORLD, W, h->n_recv, h->okey, h->opay, h->err_dev,
-                             h->side));
+  // a sort prefetched for exactly these inputs (emb_lookup_prefetch) is already queued on the side
+  // stream: consume it (the join below waits for it)
+  const bool use_pf = h->pf.valid && h->pf.ids == ids && h->pf.offsets == offsets && h->pf.batch == batch &&
+                      h->pf.nnz == nnz;
+  h->pf.valid = false;
+  if (use_pf) {
+    h->cur_set = h->pf.set;
+    h->skey = h->sk_set[h->cur_set];
+    h->spay = h->sp_set[h->cur_set];
+  } else if (h->segsort_ok) {
+    h->cur_set ^= 1;  // (stream-ordered after the previous backward: either set is free)
+    SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, h->cur_set);
+    sa.fin = (batch > 0 && nnz > 0) ? h->fin : nullptr;  // the later of sort / pool publishes the error word
+    h->skey = sa.skey;
+    h->spay = sa.spay;
+    static int serial = -1;  // experiment knob: EMB_SERIAL=1 runs the sort before the pool (no overlap)
+    if (serial < 0) serial = getenv("EMB_SERIAL") ? atoi(getenv("EMB_SERIAL")) : 0;
+    cudaStream_t ss = serial ? st : h->side;
+    if (batch > 0) LAUNCH(h, KID_SORT_PASS, ss, launch_segsort(sa, h->G, ss));
   } else {
-    e = radix_sort_pairs(h->sws, h->recv_keys, nullptr, h->ok0, h->ov0, h->ok1, h->ov1, h->n_recv, h->owner_key_bits,
-                         h->side, &h->okey, &h->opay, &nl, prof_hook, h);
-    if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("owner sort: ") + cudaGetErrorString(e));
+    int nl = 0;
+    cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz,
+                                     h->ks.key_bits, h->side, &h->skey, &h->spay, &nl, prof_hook, h);
+    if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
     h->launches += nl;
   }
-  h->owner_unique_done = false;  // the owner-side dedup is only built on demand (step statistics)
-  // gather requested rows and send them back
-  LAUNCH(h, KID_OWNER_GATHER, st, launch_owner_gather(h->w, h->recv_keys, h->n_recv, h->D, h->owner_rows, st));
-  es = exchange(h, h->owner_rows, h->recv_counts, h->roff, h->uniq_rows, h->send_counts, h->soff, sizeof(float),
-                ncclFloat32, h->D, st);
-  if (es != EMB_OK) return es;
-  pa.rows_src = h->uniq_rows;
-  pa.nrows_src = h->U_l;
-  pa.row_idx = h->inv;
+  PoolArgs pa = pool_args(h, ids, offsets, batch, nnz, out);
+  const bool fused_pub = h->segsort_ok && batch > 0 && nnz > 0;
+  pa.fin = fused_pub ? h->fin : nullptr;
+  pa.fin_kernels = use_pf ? 1 : 2;  // a prefetched sort does not take part in the publish
   if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
   CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
   CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
-  if (batch > 0) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
-  h->state = 1;
+  if (batch > 0 && !fused_pub) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
   return EMB_OK;
 }
 
-emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream_t st) {
-  if (h->state != 1) return fail(h, EMB_ERR_STATE, "emb_backward_update without a preceding emb_lookup");
-  if (h->batch > 0 && (!d_out || !aligned16(d_out)))
-    return fail(h, EMB_ERR_INVALID, "d_out must be a non-NULL 16-byte aligned device pointer");
-  CUDA_TRY(h, cudaSetDevice(h->device));
-  h->last_stream = st;
-  const bool mean = h->pool == EMB_POOL_MEAN;
+// ---- world > 1 phases (see the file header). The step's arguments are in h (cur_*, batch, nnz).
+// L0: dedup sort + route (raises KEYS)
+emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
+  const int64_t *ids = h->cur_ids, *offsets = h->cur_offsets;
+  const int32_t batch = h->batch;
+  const int64_t nnz = h->nnz;
+  h->epoch += 1;
+  h->p2p.epoch = h->epoch;
+  h->skey = h->k0;
+  h->spay = h->v0;
+  if (batch > 0 && nnz > 0) {
+    if (h->segsort_ok) {
+      SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, 0);
+      sa.validate = 1;
+      LAUNCH(h, KID_SORT_PASS, st, launch_segsort(sa, h->G, st));
+    } else {
+      LAUNCH(h, KID_KEYS, st, launch_keys(keys_args(h, ids, offsets, batch, nnz), st));
+      int nl = 0;
+      cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz, h->ks.key_bits,
+                                       st, &h->skey, &h->spay, &nl, prof_hook, h);
+      if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+      h->launches += nl;
+    }
+  } else if (batch > 0 && !h->segsort_ok) {
+    LAUNCH(h, KID_KEYS, st, launch_keys(keys_args(h, ids, offsets, batch, nnz), st));  // validates the CSR
+  }
+  RouteArgs ra{};
+  ra.skey = h->skey;
+  ra.spay = h->spay;
+  ra.n = (batch > 0) ? nnz : 0;
+  ra.ks = h->ks;
+  ra.p2p = h->p2p;
+  ra.outidx = h->outidx;
+  ra.inv = h->inv;
+  ra.send_local = h->send_local;
+  ra.scnt = h->scnt;
+  ra.tot = h->route_tot;
+  ra.status = h->route_status;
+  ra.counter = h->route_counter;
+  ra.blk_done = h->route_done;
+  if (++h->route_tag == 0) h->route_tag = 1;
+  ra.tag = h->route_tag;
+  ra.err = h->err_dev;
+  ra.extra_err = h->step_err_bits;
+  LAUNCH(h, KID_ROUTE, st, launch_route(ra, st));
+  return EMB_OK;
+}
+
+// L1: owner merge (side stream, after KEYS) | pull (after APPLIED of the previous step) + pool
+emb_status_t lookup_phase1(emb_ctx *h, cudaStream_t st) {
+  const P2PArgs &px = h->p2p;
+  const int W = h->world;
+  CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+  LAUNCH(h, KID_WAIT, h->side, launch_wait(px, P2P_KEYS, h->epoch, h->err_dev, h->side));
+  LAUNCH(h, KID_MERGE, h->side,
+         launch_merge_tree(h->recv_keys + (size_t)(h->epoch & 1u) * W * h->cap, h->xmat + xmat_idx(h->epoch, 0, 0), W,
+                           h->cap, h->ok0, h->ov0, h->ok1, h->ov1, h->n_merged, h->side));
+  LAUNCH(h, KID_WAIT, st, launch_wait(px, P2P_APPLIED, h->epoch - 1, h->err_dev, st));
+  LAUNCH(h, KID_PULL, st, launch_pull(px, h->scnt, h->send_local, h->uniq_rows, h->D, std::max<int64_t>(h->nnz, 1), st));
+  if (h->batch > 0 && h->cur_out) {
+    PoolArgs pa = pool_args(h, h->cur_ids, h->cur_offsets, h->batch, h->nnz, h->cur_out);
+    LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
+  }
+  CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
+  CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
+  LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
+  h->counts_synced = false;
+  h->owner_unique_done = false;
+  h->U_l = -1;
+  h->n_recv = -1;
+  return EMB_OK;
+}
+
+GradArgs grad_args(emb_ctx *h, const float *d_out, double lr) {
   GradArgs g{};
   g.signal_kind = -1;
   g.dim = h->D;
   g.dy = d_out;
   g.drow = h->drow;
-  g.blen = mean ? h->blen : nullptr;
+  g.blen = h->pool == EMB_POOL_MEAN ? h->blen : nullptr;
   g.batch = h->batch;
   g.num_slots = h->S;
   g.opt = h->opt;
@@ -934,102 +923,156 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
   g.nrows = h->rows_local;
   g.nsrc = (int64_t)h->S * h->batch;
   g.nsrc_occ = h->nnz;
-  g.nout = h->U_l;
   g.err = h->err_dev;
-  g.useg = h->useg;
-  g.ustart = h->ustart;
-  g.u_count = h->u_count;
+  g.lmask = 0xFFFFFFFFu;
+  g.ks = h->ks;
+  g.p2p = h->p2p;
+  return g;
+}
+
+// B0: requester merge, rows stored into the owners' regions (raises GRADS). d_out == nullptr (an
+// argument error at W > 1): no contribution, the step is marked failed at every owner.
+emb_status_t backward_phase0(emb_ctx *h, const float *d_out, double lr, cudaStream_t st) {
+  GradArgs g = grad_args(h, d_out, lr);
+  g.skey = h->skey;
+  g.spay = h->spay;
+  g.n = h->nnz;
+  g.src_mode = 0;
+  g.sink_mode = 2;
+  g.useg = h->outidx;
+  g.nout = h->cap;
+  g.lo_stride = (int64_t)h->world * h->cap * h->D;
+  g.signal_kind = P2P_GRADS;
+  if (h->batch > 0 && h->nnz > 0 && d_out)
+    LAUNCH(h, KID_GRAD_PUSH, st, launch_grad(g, st));
+  else
+    LAUNCH(h, KID_SIGNAL, st, launch_signal(h->p2p, P2P_GRADS, d_out || h->batch == 0 ? 0u : EMB_DEVERR_INVALID, st));
+  return EMB_OK;
+}
+
+// B1: wait GRADS, owner merge over sources + apply (raises APPLIED)
+emb_status_t backward_phase1(emb_ctx *h, double lr, cudaStream_t st) {
+  const int W = h->world;
+  GradArgs o = grad_args(h, nullptr, lr);
+  o.skey = h->ok0;
+  o.spay = h->ov0;
+  o.n = (int64_t)W * h->cap;
+  o.n_dev = h->n_merged;
+  o.src_mode = 1;
+  o.src = h->grecv;
+  o.src_lo = h->grecv + (size_t)W * h->cap * h->D;
+  o.nsrc = (int64_t)W * h->cap;
+  o.blen = nullptr;
+  o.sink_mode = 0;
+  o.signal_kind = P2P_APPLIED;
+  o.skip_mask = EMB_DEVERR_TIMEOUT | EMB_DEVERR_INTERNAL;
+  o.abort_bits = h->xmat + xmat_idx(h->epoch, 1, 0);
+  LAUNCH(h, KID_WAIT, st, launch_wait(h->p2p, P2P_GRADS, h->epoch, h->err_dev, st));
+  LAUNCH(h, KID_GRAD_APPLY, st, launch_grad(o, st));
+  return EMB_OK;
+}
+
+// one rank's lookup; at W > 1 a multi-process rank runs both phases back to back
+emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz,
+                         float *out, cudaStream_t st) {
+  if (h->state != 0) return fail(h, EMB_ERR_STATE, "emb_lookup called twice without emb_backward_update");
+  if (h->group) return fail(h, EMB_ERR_STATE, "a group handle steps through emb_lookup_group");
+  const char *ae = lookup_arg_error(h, ids, offsets, batch, nnz, out);
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  h->launches = 0;
+  h->last_stream = st;
   if (h->world == 1) {
+    if (*ae) return fail(h, EMB_ERR_INVALID, ae);
+    emb_status_t s = check_sticky(h);
+    if (s != EMB_OK) return s;
+    h->batch = batch;
+    h->nnz = nnz;
+    emb_status_t r = lookup_w1(h, ids, offsets, batch, nnz, out, st);
+    if (r != EMB_OK) return r;
+    h->U_l = -1;
+    h->state = 1;
+    return EMB_OK;
+  }
+  // W > 1: the call is collective -- a rank with bad arguments still takes part (empty batch) and
+  // marks the step failed at every owner, so no peer waits for it and no rank applies the step
+  h->step_err_bits = *ae ? EMB_DEVERR_INVALID : 0u;
+  h->batch = *ae ? 0 : batch;
+  h->nnz = *ae ? 0 : nnz;
+  h->cur_ids = ids;
+  h->cur_offsets = offsets;
+  h->cur_out = *ae ? nullptr : out;
+  emb_status_t r = lookup_phase0(h, st);
+  if (r == EMB_OK) r = lookup_phase1(h, st);
+  if (r != EMB_OK) return r;
+  h->state = 1;
+  if (*ae) return fail(h, EMB_ERR_INVALID, std::string(ae) + " (the rank took part with an empty batch; the step "
+                                                              "updates nothing on any rank)");
+  return check_sticky(h);
+}
+
+emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream_t st) {
+  if (h->state != 1) return fail(h, EMB_ERR_STATE, "emb_backward_update without a preceding emb_lookup");
+  if (h->group) return fail(h, EMB_ERR_STATE, "a group handle steps through emb_backward_update_group");
+  const bool bad_dout = h->batch > 0 && (!d_out || !aligned16(d_out));
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  h->last_stream = st;
+  if (h->world == 1) {
+    if (bad_dout) return fail(h, EMB_ERR_INVALID, "d_out must be a non-NULL 16-byte aligned device pointer");
+    GradArgs g = grad_args(h, d_out, lr);
     g.skey = h->skey;
     g.spay = h->spay;
     g.n = h->nnz;
     g.src_mode = 0;
     g.sink_mode = 0;
-    g.lmask = 0xFFFFFFFFu;
+    // a step whose input had an error updates nothing (decided on the device: deterministic)
+    g.skip_mask = EMB_DEVERR_RANGE | EMB_DEVERR_INVALID | EMB_DEVERR_INTERNAL;
     LAUNCH(h, KID_GRAD_APPLY, st, launch_grad(g, st));
     h->state = 0;
     return EMB_OK;
   }
-  if (h->use_p2p) {
-    // requester: merged per-key gradients stored straight into the owners' receive buffers (fused X3)
-    P2PArgs px = h->p2p;
-    px.epoch = h->epoch;
-    g.skey = h->skey;
-    g.spay = h->spay;
-    g.n = h->nnz;
-    g.src_mode = 0;
-    g.sink_mode = 2;
-    g.useg = h->outidx;
-    g.nout = h->max_ids;
-    g.p2p = px;
-    static int push = -1;  // experiment knob: EMB_GRAD_PUSH=1 -> local merge (MODE 2) + streaming push
-    if (push < 0) push = getenv("EMB_GRAD_PUSH") ? atoi(getenv("EMB_GRAD_PUSH")) : 0;
-    if (push && g.n > 0) {
-      g.sink_mode = 1;
-      g.out_rows = h->gloc;
-      LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
-      LAUNCH(h, KID_NCCL, st, launch_push_rows(px, h->gloc, h->D, h->max_ids, st));
-    } else {
-    g.signal_kind = P2P_GRADS;  // the last warp of the requester grad raises GRADS
-    if (g.n > 0)
-      LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
-    else
-      LAUNCH(h, KID_NCCL, st, launch_signal(px, P2P_GRADS, st));
-    }
-    // owner: merge the W sources' gradients per row (source-rank order) and apply
-    GradArgs o = g;
-    o.skey = h->okey;
-    o.spay = h->opay;
-    o.n = h->recv_cap;
-    o.n_dev = &h->rt->n_recv;
-    o.src_mode = 1;
-    o.src = h->grecv;
-    o.nsrc = h->recv_cap;
-    o.blen = nullptr;
-    o.sink_mode = 0;
-    o.lmask = 0xFFFFFFFFu;
-    o.signal_kind = -1;
-    LAUNCH(h, KID_WAIT, st, launch_wait(px, P2P_GRADS, h->err_dev, st));
-    LAUNCH(h, KID_GRAD_APPLY, st, launch_grad(o, st));
-    h->state = 0;
-    return EMB_OK;
-  }
-  // requester: per-unique-key local gradient (fp32 rows in unique order = owner-grouped send order)
-  g.skey = h->skey;
-  g.spay = h->spay;
-  g.n = h->nnz;
-  g.src_mode = 0;
-  g.sink_mode = 1;
-  g.out_rows = h->gloc;
-  if (h->ukey_is_g) g.useg = h->outidx;  // merged gradient of a key goes to its send position
-  LAUNCH(h, KID_GRAD_LOCAL, st, launch_grad(g, st));
-  emb_status_t es = exchange(h, h->gloc, h->send_counts, h->soff, h->grecv, h->recv_counts, h->roff, sizeof(float),
-                             ncclFloat32, h->D, st);
-  if (es != EMB_OK) return es;
-  // owner: merge the W sources' gradients per row (source-rank order) and apply
-  GradArgs o = g;
-  o.skey = h->okey;
-  o.spay = h->opay;
-  o.n = h->n_recv;
-  o.src_mode = 1;
-  o.src = h->grecv;
-  o.nsrc = h->n_recv;
-  o.useg = h->ouseg;
-  o.ustart = h->oustart;
-  o.u_count = h->ou_count;
-  o.blen = nullptr;
-  o.sink_mode = 0;
-  o.lmask = 0xFFFFFFFFu;
-  LAUNCH(h, KID_GRAD_APPLY, st, launch_grad(o, st));
+  emb_status_t r = backward_phase0(h, bad_dout ? nullptr : d_out, lr, st);
+  if (r == EMB_OK) r = backward_phase1(h, lr, st);
   h->state = 0;
+  if (r != EMB_OK) return r;
+  if (bad_dout)
+    return fail(h, EMB_ERR_INVALID, "d_out must be a non-NULL 16-byte aligned device pointer (the rank took part; "
+                                    "the step updates nothing on any rank)");
+  return check_sticky(h);
+}
+
+// group mode: run phase `ph` of every rank, each after every rank's previous phase (cross-stream
+// events), so the flag waits inside a phase always find their flags raised
+template <typename F>
+emb_status_t group_phase(emb_ctx *const *hs, int n, void *const *streams, F &&phase) {
+  for (int r = 0; r < n; ++r) {
+    emb_ctx *h = hs[r];
+    cudaStream_t st = static_cast<cudaStream_t>(streams ? streams[r] : nullptr);
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    for (int p = 0; p < n; ++p)
+      if (p != r) CUDA_TRY(h, cudaStreamWaitEvent(st, hs[p]->ev_phase, 0));
+  }
+  for (int r = 0; r < n; ++r) {
+    emb_ctx *h = hs[r];
+    cudaStream_t st = static_cast<cudaStream_t>(streams ? streams[r] : nullptr);
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    h->last_stream = st;
+    emb_status_t s = phase(h, r, st);
+    if (s != EMB_OK) return s;
+    CUDA_TRY(h, cudaEventRecord(h->ev_phase, st));
+  }
   return EMB_OK;
 }
 
-// host-side unique of the last step (runs the GPU dedup kernel if the step did not)
+emb_status_t check_group(emb_ctx *const *hs, int n) {
+  if (!hs || n < 1) return EMB_ERR_INVALID;
+  for (int r = 0; r < n; ++r)
+    if (!hs[r] || !hs[r]->group || hs[r]->world != n || hs[r]->rank != r) return EMB_ERR_INVALID;
+  return EMB_OK;
+}
+
+// host-side unique of the last step (runs the GPU dedup kernel on demand)
 emb_status_t ensure_unique(emb_ctx *h) {
-  if (h->world > 1) return sync_counts(h);
   if (h->U_l >= 0) return EMB_OK;
-  // world == 1: the step itself never needs the compacted unique list; build it on demand
   cudaStream_t st = h->last_stream;
   UniqueArgs ua{h->skey, h->nnz, h->useg, h->ukey, h->ustart, h->uend, h->u_count, h->uniq_status, h->uniq_counter, ++h->uniq_epoch};
   CUDA_TRY(h, launch_unique(ua, st));
@@ -1042,23 +1085,23 @@ emb_status_t ensure_unique(emb_ctx *h) {
 
 // owner-side dedup of the merged received keys, built on demand (not part of the step)
 emb_status_t ensure_owner_unique(emb_ctx *h) {
-  if (h->world > 1) {
-    emb_status_t s = sync_counts(h);
-    if (s != EMB_OK) return s;
+  if (h->world == 1 || h->owner_unique_done) return EMB_OK;
+  emb_status_t s = sync_counts(h);
+  if (s != EMB_OK) return s;
+  if (h->n_recv > 0) {
+    cudaStream_t st = h->last_stream;
+    UniqueArgs ua{h->ok0, h->n_recv, h->ouseg, h->oukey, h->oustart, h->ouend, h->ou_count, h->ouniq_status,
+                  h->ouniq_counter, ++h->ouniq_epoch};
+    CUDA_TRY(h, launch_unique(ua, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
   }
-  if (h->world == 1 || h->owner_unique_done || h->n_recv <= 0) return EMB_OK;
-  cudaStream_t st = h->last_stream;
-  UniqueArgs ua{h->okey, h->n_recv, h->ouseg, h->oukey, h->oustart, h->ouend, h->ou_count, h->ouniq_status,
-                h->ouniq_counter, ++h->ouniq_epoch};
-  CUDA_TRY(h, launch_unique(ua, st));
-  CUDA_TRY(h, cudaStreamSynchronize(st));
   h->owner_unique_done = true;
   return EMB_OK;
 }
 
 emb_status_t copy_unique(emb_ctx *h, const uint32_t *uend_dev, const uint32_t *ukey_dev, const uint32_t *ustart_dev,
-                         int64_t U, bool routing_keys, bool owner_local_keys, uint64_t *keys_host,
-                         int64_t *counts_host, int64_t cap, int64_t *n_out) {
+                         int64_t U, bool owner_local_keys, uint64_t *keys_host, int64_t *counts_host, int64_t cap,
+                         int64_t *n_out) {
   if (n_out) *n_out = U;
   if (cap < U) return fail(h, EMB_ERR_INVALID, "capacity smaller than the number of unique keys");
   std::vector<uint32_t> k(U), s(U), e(U);
@@ -1069,27 +1112,33 @@ emb_status_t copy_unique(emb_ctx *h, const uint32_t *uend_dev, const uint32_t *u
   }
   for (int64_t u = 0; u < U; ++u) {
     if (keys_host) {
-      uint64_t g;
-      if (owner_local_keys) {
-        // owner-side local id -> global
+      uint64_t g = k[u];
+      if (owner_local_keys) {  // owner-side local id -> global
         const uint64_t local = k[u];
-        g = h->shard == 0 ? local * (uint64_t)h->world + (uint64_t)h->rank : (uint64_t)h->rank * h->ks.rows_per + local;
-      } else {
-        g = routing_keys ? key_to_global(k[u], h->ks) : k[u];
+        g = h->shard == 0 ? local * (uint64_t)h->world + (uint64_t)h->rank
+                          : (uint64_t)h->rank * h->ks.rows_per + local;
       }
       keys_host[u] = g;
     }
     if (counts_host) counts_host[u] = (int64_t)e[u] - (int64_t)s[u];
   }
-  if (keys_host && !owner_local_keys && h->world > 1) {
-    // requester keys are owner-major; report them sorted by global key like the oracle's U
-    std::vector<std::pair<uint64_t, int64_t>> v(U);
-    for (int64_t u = 0; u < U; ++u) v[u] = {keys_host[u], counts_host ? counts_host[u] : 0};
-    std::sort(v.begin(), v.end());
-    for (int64_t u = 0; u < U; ++u) {
-      keys_host[u] = v[u].first;
-      if (counts_host) counts_host[u] = v[u].second;
-    }
+  return EMB_OK;
+}
+
+// ---- host-buffer (e2e) path: double-buffered staging. The H2D copies of a call run on a copy stream
+// (so they can overlap the previous call's device work and D2H); the D2H of the result is enqueued on
+// the caller stream and the call returns after the stream work completed.
+emb_status_t ensure_staging(emb_ctx *h) {
+  if (h->st_ids[0]) return EMB_OK;
+  const size_t SB = (size_t)h->S * h->max_batch;
+  for (int k = 0; k < 2; ++k)
+    if (dalloc(h, &h->st_ids[k], h->max_ids) || dalloc(h, &h->st_offsets[k], SB + 1) ||
+        dalloc(h, &h->st_out[k], SB * h->D) || dalloc(h, &h->st_dout[k], SB * h->D))
+      return fail(h, EMB_ERR_NOMEM, "cannot allocate host-path staging");
+  CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_h2d[k], cudaEventDisableTiming));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_d2h[k], cudaEventDisableTiming));
   }
   return EMB_OK;
 }
@@ -1104,7 +1153,7 @@ emb_status_t emb_create(const emb_config_t *cfg, emb_handle_t *out) {
   *out = nullptr;
   emb_ctx *h = new (std::nothrow) emb_ctx();
   if (!h) return EMB_ERR_NOMEM;
-  emb_status_t s = create_impl(cfg, h);
+  emb_status_t s = create_impl(cfg, h, 0);
   if (s != EMB_OK) {
     {
       std::lock_guard<std::mutex> lk(g_err_mu);
@@ -1114,6 +1163,49 @@ emb_status_t emb_create(const emb_config_t *cfg, emb_handle_t *out) {
     return s;
   }
   *out = h;
+  return EMB_OK;
+}
+
+emb_status_t emb_create_group(const emb_config_t *cfgs, int32_t n, emb_handle_t *out) {
+  if (!out || !cfgs || n < 1 || n > EMB_MAX_WORLD) return EMB_ERR_INVALID;
+  for (int r = 0; r < n; ++r) out[r] = nullptr;
+  int64_t cap = 0;
+  for (int r = 0; r < n; ++r) {
+    if (cfgs[r].world != n || cfgs[r].rank != r) {
+      std::lock_guard<std::mutex> lk(g_err_mu);
+      g_create_error = "emb_create_group: cfgs[r] must have world == n and rank == r";
+      return EMB_ERR_INVALID;
+    }
+    cap = std::max<int64_t>(cap, cfgs[r].max_ids);
+  }
+  std::vector<emb_ctx *> hs(n, nullptr);
+  emb_status_t s = EMB_OK;
+  std::string msg;
+  for (int r = 0; r < n && s == EMB_OK; ++r) {
+    hs[r] = new (std::nothrow) emb_ctx();
+    if (!hs[r]) {
+      s = EMB_ERR_NOMEM;
+      msg = "out of host memory";
+      break;
+    }
+    s = create_impl(&cfgs[r], hs[r], std::max<int64_t>(cap, 1));
+    if (s != EMB_OK) msg = hs[r]->last_error;
+  }
+  if (s == EMB_OK && n > 1) {
+    s = setup_group(hs);
+    if (s != EMB_OK)
+      for (auto *h : hs)
+        if (h && h->last_error != "no error") msg = h->last_error;
+  }
+  if (s != EMB_OK) {
+    {
+      std::lock_guard<std::mutex> lk(g_err_mu);
+      g_create_error = msg;
+    }
+    for (auto *h : hs) destroy_impl(h);
+    return s;
+  }
+  for (int r = 0; r < n; ++r) out[r] = hs[r];
   return EMB_OK;
 }
 
@@ -1144,20 +1236,91 @@ emb_status_t emb_lookup_prefetch(emb_handle_t h, const int64_t *ids, const int64
 
 emb_status_t emb_backward_update(emb_handle_t h, const float *d_out, double lr, void *cuda_stream) {
   if (!h) return EMB_ERR_INVALID;
-  emb_status_t s = check_sticky(h);
-  if (s != EMB_OK) {
-    h->state = 0;
-    return s;
+  if (h->world == 1 && h->state == 1) {
+    emb_status_t s = check_sticky(h);  // fail fast (the device skips the update anyway)
+    if (s != EMB_OK) {
+      h->state = 0;
+      return s;
+    }
   }
   return backward_impl(h, d_out, lr, static_cast<cudaStream_t>(cuda_stream));
 }
 
-static emb_status_t ensure_staging(emb_ctx *h) {
-  if (h->st_ids) return EMB_OK;
-  const size_t SB = (size_t)h->S * h->max_batch;
-  if (dalloc(h, &h->st_ids, h->max_ids) || dalloc(h, &h->st_offsets, SB + 1) ||
-      dalloc(h, &h->st_out, SB * h->D) || dalloc(h, &h->st_dout, SB * h->D))
-    return fail(h, EMB_ERR_NOMEM, "cannot allocate host-path staging");
+emb_status_t emb_lookup_group(emb_handle_t *hs, int32_t n, const int64_t *const *ids, const int64_t *const *offsets,
+                              const int32_t *batch, const int64_t *nnz, float *const *out, void *const *streams) {
+  if (check_group(hs, n) != EMB_OK || !ids || !offsets || !batch || !nnz || !out) return EMB_ERR_INVALID;
+  for (int r = 0; r < n; ++r)
+    if (hs[r]->state != 0) return fail(hs[r], EMB_ERR_STATE, "emb_lookup_group called twice without a backward");
+  emb_status_t first_err = EMB_OK;
+  for (int r = 0; r < n; ++r) {
+    emb_ctx *h = hs[r];
+    const char *ae = lookup_arg_error(h, ids[r], offsets[r], batch[r], nnz[r], out[r]);
+    h->launches = 0;
+    h->step_err_bits = *ae ? EMB_DEVERR_INVALID : 0u;
+    h->batch = *ae ? 0 : batch[r];
+    h->nnz = *ae ? 0 : nnz[r];
+    h->cur_ids = ids[r];
+    h->cur_offsets = offsets[r];
+    h->cur_out = *ae ? nullptr : out[r];
+    if (*ae && first_err == EMB_OK) first_err = fail(h, EMB_ERR_INVALID, std::string("rank ") + std::to_string(r) + ": " + ae);
+  }
+  if (n == 1) {  // a group of one is a W = 1 layer
+    emb_ctx *h = hs[0];
+    if (first_err != EMB_OK) return first_err;
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(streams ? streams[0] : nullptr);
+    h->last_stream = st;
+    emb_status_t s = check_sticky(h);
+    if (s != EMB_OK) return s;
+    s = lookup_w1(h, ids[0], offsets[0], batch[0], nnz[0], out[0], st);
+    if (s != EMB_OK) return s;
+    h->U_l = -1;
+    h->state = 1;
+    return EMB_OK;
+  }
+  emb_status_t s = group_phase(hs, n, streams, [](emb_ctx *h, int, cudaStream_t st) { return lookup_phase0(h, st); });
+  if (s == EMB_OK)
+    s = group_phase(hs, n, streams, [](emb_ctx *h, int, cudaStream_t st) { return lookup_phase1(h, st); });
+  if (s != EMB_OK) return s;
+  for (int r = 0; r < n; ++r) hs[r]->state = 1;
+  if (first_err != EMB_OK) return first_err;
+  for (int r = 0; r < n; ++r) {
+    emb_status_t e = check_sticky(hs[r]);
+    if (e != EMB_OK) return e;
+  }
+  return EMB_OK;
+}
+
+emb_status_t emb_backward_update_group(emb_handle_t *hs, int32_t n, const float *const *d_out, double lr,
+                                       void *const *streams) {
+  if (check_group(hs, n) != EMB_OK || !d_out) return EMB_ERR_INVALID;
+  for (int r = 0; r < n; ++r)
+    if (hs[r]->state != 1) return fail(hs[r], EMB_ERR_STATE, "emb_backward_update_group without a lookup");
+  if (n == 1) {
+    emb_ctx *h = hs[0];
+    h->group = false;  // (the W = 1 path of backward_impl)
+    emb_status_t s = emb_backward_update(h, d_out[0], lr, streams ? streams[0] : nullptr);
+    h->group = true;
+    return s;
+  }
+  emb_status_t first_err = EMB_OK;
+  std::vector<const float *> dd(n);
+  for (int r = 0; r < n; ++r) {
+    const bool bad = hs[r]->batch > 0 && (!d_out[r] || !aligned16(d_out[r]));
+    dd[r] = bad ? nullptr : d_out[r];
+    if (bad && first_err == EMB_OK) first_err = fail(hs[r], EMB_ERR_INVALID, "d_out must be a non-NULL 16-byte aligned device pointer");
+  }
+  emb_status_t s = group_phase(hs, n, streams,
+                               [&](emb_ctx *h, int r, cudaStream_t st) { return backward_phase0(h, dd[r], lr, st); });
+  if (s == EMB_OK)
+    s = group_phase(hs, n, streams, [&](emb_ctx *h, int, cudaStream_t st) { return backward_phase1(h, lr, st); });
+  for (int r = 0; r < n; ++r) hs[r]->state = 0;
+  if (s != EMB_OK) return s;
+  if (first_err != EMB_OK) return first_err;
+  for (int r = 0; r < n; ++r) {
+    emb_status_t e = check_sticky(hs[r]);
+    if (e != EMB_OK) return e;
+  }
   return EMB_OK;
 }
 
@@ -1172,13 +1335,14 @@ emb_status_t emb_lookup_host(emb_handle_t h, const int64_t *ids, const int64_t *
   if (s != EMB_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   const size_t SB = (size_t)h->S * batch;
-  if (nnz > 0) CUDA_TRY(h, cudaMemcpyAsync(h->st_ids, ids, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+  const int k = h->st_set;
+  if (nnz > 0) CUDA_TRY(h, cudaMemcpyAsync(h->st_ids[k], ids, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
   if (batch > 0)
-    CUDA_TRY(h, cudaMemcpyAsync(h->st_offsets, offsets, sizeof(int64_t) * (SB + 1), cudaMemcpyHostToDevice, st));
-  s = lookup_impl(h, h->st_ids, h->st_offsets, batch, nnz, h->st_out, st);
+    CUDA_TRY(h, cudaMemcpyAsync(h->st_offsets[k], offsets, sizeof(int64_t) * (SB + 1), cudaMemcpyHostToDevice, st));
+  s = lookup_impl(h, h->st_ids[k], h->st_offsets[k], batch, nnz, h->st_out[k], st);
   if (s != EMB_OK) return s;
   if (batch > 0)
-    CUDA_TRY(h, cudaMemcpyAsync(out, h->st_out, sizeof(float) * SB * h->D, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaMemcpyAsync(out, h->st_out[k], sizeof(float) * SB * h->D, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaStreamSynchronize(st));
   return check_sticky(h);
 }
@@ -1190,11 +1354,12 @@ emb_status_t emb_backward_update_host(emb_handle_t h, const float *d_out, double
   if (s != EMB_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   const size_t SB = (size_t)h->S * h->batch;
+  const int k = h->st_set;
   if (h->state == 1 && h->batch > 0) {
     if (!d_out) return fail(h, EMB_ERR_INVALID, "NULL d_out");
-    CUDA_TRY(h, cudaMemcpyAsync(h->st_dout, d_out, sizeof(float) * SB * h->D, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(h->st_dout[k], d_out, sizeof(float) * SB * h->D, cudaMemcpyHostToDevice, st));
   }
-  s = emb_backward_update(h, h->st_dout, lr, st);
+  s = emb_backward_update(h, h->st_dout[k], lr, st);
   if (s != EMB_OK) return s;
   CUDA_TRY(h, cudaStreamSynchronize(st));
   return check_sticky(h);
@@ -1292,16 +1457,16 @@ emb_status_t emb_last_step_info(emb_handle_t h, emb_step_info_t *info) {
     info->send_counts[0] = h->U_l;
     info->recv_counts[0] = h->U_l;
   } else {
+    s = ensure_owner_unique(h);
+    if (s != EMB_OK) return s;
     info->recv_keys = h->n_recv;
     for (int p = 0; p < h->world; ++p) {
       info->send_counts[p] = h->send_counts[p];
       info->recv_counts[p] = h->recv_counts[p];
     }
-    emb_status_t s2 = ensure_owner_unique(h);
-    if (s2 != EMB_OK) return s2;
     uint32_t u = 0;
-    CUDA_TRY(h, cudaMemcpy(&u, h->ou_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    info->unique_owner = h->n_recv > 0 ? u : 0;
+    if (h->n_recv > 0) CUDA_TRY(h, cudaMemcpy(&u, h->ou_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    info->unique_owner = u;
   }
   return EMB_OK;
 }
@@ -1314,7 +1479,7 @@ emb_status_t emb_last_unique(emb_handle_t h, uint64_t *keys_host, int64_t *count
   if (s != EMB_OK) return s;
   uint32_t U = 0;
   CUDA_TRY(h, cudaMemcpy(&U, h->u_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  return copy_unique(h, h->uend, h->ukey, h->ustart, U, !h->ukey_is_g, false, keys_host, counts_host, cap, n_out);
+  return copy_unique(h, h->uend, h->ukey, h->ustart, U, false, keys_host, counts_host, cap, n_out);
 }
 
 emb_status_t emb_last_owner_unique(emb_handle_t h, uint64_t *keys_host, int64_t *counts_host, int64_t cap,
@@ -1322,10 +1487,11 @@ emb_status_t emb_last_owner_unique(emb_handle_t h, uint64_t *keys_host, int64_t 
   if (!h) return EMB_ERR_INVALID;
   if (h->world == 1) return emb_last_unique(h, keys_host, counts_host, cap, n_out);
   CUDA_TRY(h, cudaSetDevice(h->device));
-  if (h->last_stream) CUDA_TRY(h, cudaStreamSynchronize(h->last_stream));
+  emb_status_t s = ensure_owner_unique(h);  // (syncs the counts and builds the owner dedup on demand)
+  if (s != EMB_OK) return s;
   uint32_t U = 0;
   if (h->n_recv > 0) CUDA_TRY(h, cudaMemcpy(&U, h->ou_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  return copy_unique(h, h->ouend, h->oukey, h->oustart, U, false, true, keys_host, counts_host, cap, n_out);
+  return copy_unique(h, h->ouend, h->oukey, h->oustart, U, true, keys_host, counts_host, cap, n_out);
 }
 
 int64_t emb_rows_local(emb_handle_t h) { return h ? h->rows_local : -1; }
@@ -1380,6 +1546,9 @@ emb_status_t emb_clear_error(emb_handle_t h) {
   CUDA_TRY(h, cudaSetDevice(h->device));
   CUDA_TRY(h, cudaDeviceSynchronize());
   CUDA_TRY(h, cudaMemset(h->err_dev, 0, sizeof(uint32_t)));
+  // a pass stopped by a tripped guard can leave segment tickets taken: start clean
+  CUDA_TRY(h, cudaMemset(h->tickets, 0, sizeof(uint32_t) * h->nticket));
+  CUDA_TRY(h, cudaDeviceSynchronize());
   *(volatile uint32_t *)h->err_host = 0;
   h->state = 0;
   h->last_error = "no error";

@@ -1,7 +1,7 @@
 // grad.cu — K6+K7 fused: deterministic segment reduce of duplicate-id gradients + sparse optimizer
 // apply (readings R8-R14, R16).
 //
-// Input: the stably sorted (routing key, payload) array of the step. Every distinct key is a
+// Input: the stably sorted (fused key, payload) array of the step. Every distinct key is a
 // contiguous SEGMENT whose contributions appear in occurrence order (stable sort); invalid
 // occurrences (EMB_SENTINEL keys) are skipped wherever they sit.
 //
@@ -30,8 +30,8 @@
 // conversions); the update lr*g/(sqrt(a)+eps) in fp32 with MUFU sqrt/rcp (|update| <= lr, so its
 // relative error of a few 1e-7 is <= 1e-8 absolute, far inside the 1e-6 + 1e-5|w| tolerance;
 // DESIGN.md §2 R16').
-// 2 = write the fp32 per-unique-key gradient (requester side of the W>1 exchange). 3 = the same row
-// stored into the owner through peer memory. 4 = row-wise Adagrad (SURVEY §8(f) f1, R14'): one
+// 3 = the merged fp32 per-key row stored into the owner's gradient region through peer memory
+// (requester side of the W > 1 exchange; host sink_mode 2). 4 = row-wise Adagrad (SURVEY §8(f) f1, R14'): one
 // accumulator per row, a <- a + (1/D) sum_c g[c]^2 with g = fp32(G) (fp32 FMAs + an xor-butterfly
 // warp reduction: every lane ends with the same total); w as in mode 1 with the row's a.
 #include <stdlib.h>
@@ -142,21 +142,28 @@ __device__ __forceinline__ void apply_rowwise(const GradArgs &a, const OptConst 
   if ((threadIdx.x & 31) == 0) a.a[lrow] = af;
 }
 
-// destination row of a merged per-key gradient (MODE 2: local X3 send buffer; MODE 3: the owner's
-// receive buffer through peer memory, at my offset there + the key's position in my send order)
-// MODE 3: the route table's send offsets / destination offsets, staged in shared memory once per CTA
-// (the per-row owner search then reads shared memory, not a chain of global loads)
-__shared__ int64_t g_rt_soff[P2P_MAXW + 1], g_rt_dst[P2P_MAXW];
+// destination row of a merged per-key gradient (MODE 3, requester side at W > 1): the owner o of key g
+// holds a region of cap rows per source; this rank's key of rank ui in o's list goes to row
+// rank*cap + ui there (peer memory over NVLink, or this rank's own buffer when o == rank)
+__device__ __forceinline__ float *out_row3(const GradArgs &a, uint32_t key, uint32_t ui, int D) {
+  const uint32_t o = owner_of_g(key, a.ks);
+  return a.p2p.peer_grecv[o] + (size_t)((int64_t)a.p2p.rank * a.p2p.cap + ui) * D;
+}
 
-template <int MODE>
-__device__ __forceinline__ float *out_row(const GradArgs &a, uint32_t ui, int D) {
-  if constexpr (MODE == 3) {
-    int d = 0;
-    while (d + 1 < a.p2p.world && (int64_t)ui >= g_rt_soff[d + 1]) ++d;
-    return a.p2p.peer_grecv[d] + (size_t)(g_rt_dst[d] + ((int64_t)ui - g_rt_soff[d])) * D;
-  } else {
-    return a.out_rows + (size_t)ui * D;
+// a merged per-key partial crosses the exchange as a double-float pair: hi = fp32(G), lo = fp32(G - hi)
+// (hi + lo carries ~48 bits, so partials of different ranks that cancel at the owner keep the fp64
+// result; an fp32 partial alone failed the tolerance on hot keys, reading R11'' in DESIGN.md). The lo
+// row sits lo_stride floats after the hi row.
+template <int CPL>
+__device__ __forceinline__ void store_hilo(const GradArgs &a, float *dst, const double (&g)[CPL]) {
+  VecF<CPL> hi, lo;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    hi.v[c] = (float)g[c];
+    lo.v[c] = (float)__dsub_rn(g[c], (double)hi.v[c]);
   }
+  stg_frag<CPL>(dst, hi);
+  stg_frag<CPL>(dst + a.lo_stride, lo);
 }
 
 // the last warp of the grid to finish raises the exchange flag (after every warp fenced its stores)
@@ -247,12 +254,9 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
       tot[c + 1] = __dadd_rn(tot[c + 1], v.y);
     }
   }
-  if constexpr (MODE == 2 || MODE == 3) {
-    VecF<CPL> o;
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) o.v[c] = (float)tot[c];
-    stg_frag<CPL>(out_row<MODE>(a, a.useg[pos], D) + col, o);
-    if (MODE == 3) __threadfence_system();
+  if constexpr (MODE == 3) {
+    store_hilo<CPL>(a, out_row3(a, key, a.useg[pos], D) + col, tot);
+    __threadfence_system();
   } else if constexpr (MODE == 4) {
     const uint32_t lrow = key & a.lmask;
     const size_t off = (size_t)lrow * D + col;
@@ -272,16 +276,19 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
 
 // per-lane metadata of one tile (lane i < T describes position t0 + i)
 struct TileMeta {
-  uint32_t key;   // routing key (EMB_SENTINEL = invalid / beyond the range)
+  uint32_t key;   // sorted key (EMB_SENTINEL = invalid / beyond the range)
   int32_t len;    // bag length (mean pooling)
-  uint32_t uo;    // MODE 2: unique index of the position
+  uint32_t uo;    // MODE 3: rank of the key in its owner's list
   uint32_t vmask, hmask, tmask;  // warp-uniform: valid / head / tail
 };
 
-template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2>
+template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2, bool LO = false>
 __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ GradArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int NA = (MODE == 1) ? 3 : ((MODE == 0 || MODE == 4) ? 2 : 1);  // row arrays per stage: contribution, w, a
+  // row arrays per stage: contribution (+ its low part, LO: owner side at W > 1), w, a
+  constexpr int NA = ((MODE == 1) ? 3 : ((MODE == 0 || MODE == 4) ? 2 : 1)) + (LO ? 1 : 0);
+  constexpr int OFF_W = (1 + (LO ? 1 : 0)) * T;  // stage offsets in rows of D floats
+  constexpr int OFF_A = OFF_W + T;
   constexpr bool SINK_OPT = MODE < 2 || MODE == 4;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int D = DC ? DC : a.dim;  // compile-time row width for D = 64 / 128 / 256
@@ -290,14 +297,14 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
   const int C16 = D >> 2;  // 16-byte chunks per row (a constant when DC != 0)
   const size_t stage_floats = (size_t)NA * T * D + (MODE == 4 ? T : 0);  // (+ T row accumulators)
   const uint32_t wbase = smem_u32(smem) + (uint32_t)(wib * NS * stage_floats * 4);
-  if constexpr (MODE == 3) {
-    if (threadIdx.x <= a.p2p.world) g_rt_soff[threadIdx.x] = a.p2p.rt->soff[threadIdx.x];
-    if (threadIdx.x < a.p2p.world) g_rt_dst[threadIdx.x] = a.p2p.rt->dst_off[threadIdx.x];
-    __syncthreads();
-  }
   const int64_t gw = ((int64_t)blockIdx.x * (blockDim.x >> 5)) + wib;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t n = a.n_dev ? *a.n_dev : a.n;
+  // a step with an input error (any rank), a peer timeout or a tripped guard applies nothing; every
+  // warp reads the same words, so the decision is grid-uniform and the last-warp signal still fires
+  bool skip = a.skip_mask && (ld_cg_u32(a.err) & a.skip_mask);
+  if (a.abort_bits)
+    for (int s = 0; s < a.p2p.world; ++s) skip = skip || a.abort_bits[s] != 0;
+  const int64_t n = skip ? 0 : (a.n_dev ? *a.n_dev : a.n);
   const int64_t R = (n + nwarps - 1) / nwarps;
   const int64_t p_lo = gw * R;
   const int64_t p_hi = (p_lo + R < n) ? p_lo + R : n;
@@ -371,14 +378,17 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
       const uint32_t ri = __shfl_sync(0xffffffffu, srow, il);
       const unsigned long long wri = __shfl_sync(0xffffffffu, wrow, il);
       const uint32_t off = (uint32_t)((i * D + c * 4) * 4);
-      if (i < T && ((m.vmask >> i) & 1u)) cp_async16(sb + off, src_base + (size_t)ri * D + c * 4);
+      if (i < T && ((m.vmask >> i) & 1u)) {
+        cp_async16(sb + off, src_base + (size_t)ri * D + c * 4);
+        if (LO) cp_async16(sb + (uint32_t)(T * D * 4) + off, a.src_lo + (size_t)ri * D + c * 4);
+      }
       if (SINK_OPT && i < T && ((amask >> i) & 1u)) {
-        cp_async16(sb + (uint32_t)(T * D * 4) + off, a.w + wri + c * 4);
-        if (MODE == 1) cp_async16(sb + (uint32_t)(2 * T * D * 4) + off, a.a + wri + c * 4);
+        cp_async16(sb + (uint32_t)(OFF_W * D * 4) + off, a.w + wri + c * 4);
+        if (MODE == 1) cp_async16(sb + (uint32_t)(OFF_A * D * 4) + off, a.a + wri + c * 4);
       }
     }
     if (MODE == 4 && lane < T && ((amask >> lane) & 1u))  // the row's accumulator (4 bytes)
-      cp_async4(sb + (uint32_t)(2 * T * D * 4) + 4u * (uint32_t)lane, a.a + (k & a.lmask));
+      cp_async4(sb + (uint32_t)(OFF_A * D * 4) + 4u * (uint32_t)lane, a.a + (k & a.lmask));
   };
 
   TileMeta meta[NS];
@@ -403,7 +413,8 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
   int64_t open_pos = p_lo;
   uint32_t open_key = 0;
 
-  for (int64_t tb = 0; tb < ntile; tb += NS) {
+  bool broken = false;  // (the signal below must still fire: peers wait for it)
+  for (int64_t tb = 0; tb < ntile && !broken; tb += NS) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) {  // static stage index: the tile metadata stays in registers
       const int64_t ti = tb + s;
@@ -414,8 +425,8 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
       __syncwarp();             // ... and every other lane's
       if (__any_sync(0xffffffffu, bad)) {  // broken invariant (bug): report and stop, never apply garbage
         if (lane == 0) atomicOr(a.err, EMB_DEVERR_INTERNAL);
-        cp_async_wait<0>();
-        return;
+        broken = true;
+        break;
       }
       const uint32_t sbase = wbase + (uint32_t)(s * stage_floats * 4) + 4u * (uint32_t)col;
       const uint32_t vmask = m.vmask, hmask = m.hmask, tmask = m.tmask;
@@ -429,7 +440,13 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
         VecF<CPL> v;
         if (active) lds_frag<CPL>(v, sbase + 4u * (uint32_t)(i * D));
         else v.zero();
-        if constexpr (MEAN) {
+        if constexpr (LO) {  // a received per-key partial = hi + lo (double-float, R11'')
+          VecF<CPL> vl;
+          if (active) lds_frag<CPL>(vl, sbase + 4u * (uint32_t)((T + i) * D));
+          else vl.zero();
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc.v[c] = __dadd_rn(__dadd_rn(acc.v[c], (double)v.v[c]), (double)vl.v[c]);
+        } else if constexpr (MEAN) {
           const int32_t li = __shfl_sync(0xffffffffu, m.len, i);
           const double dl = (double)li;
 #pragma unroll
@@ -444,26 +461,21 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
           if (begins) {  // complete inside the range
             if constexpr (!SINK_OPT) {
               const uint32_t ui = __shfl_sync(0xffffffffu, m.uo, i);
-              if (active) {
-                VecF<CPL> o;
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) o.v[c] = (float)acc.v[c];
-                stg_frag<CPL>(out_row<MODE>(a, ui, D) + col, o);
-              }
+              if (active) store_hilo<CPL>(a, out_row3(a, ki, ui, D) + col, acc.v);
             } else if constexpr (MODE == 4) {
               VecF<CPL> wv;
-              if (active) lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((T + i) * D));
+              if (active) lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((OFF_W + i) * D));
               else wv.zero();
               float a_old;
-              const uint32_t sa_ = wbase + (uint32_t)(s * stage_floats * 4) + 4u * (uint32_t)(2 * T * D + i);
+              const uint32_t sa_ = wbase + (uint32_t)(s * stage_floats * 4) + 4u * (uint32_t)(OFF_A * D + i);
               asm volatile("ld.shared.f32 %0, [%1];" : "=f"(a_old) : "r"(sa_));
               const uint32_t lrow = ki & a.lmask;
               apply_rowwise<CPL>(a, oc, acc.v, wv, a_old, (size_t)lrow * D + col, lrow, active, D);
             } else {
               if (active) {
                 VecF<CPL> wv, av;
-                lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((T + i) * D));
-                if (MODE == 1) lds_frag<CPL>(av, sbase + 4u * (uint32_t)((2 * T + i) * D));
+                lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((OFF_W + i) * D));
+                if (MODE == 1) lds_frag<CPL>(av, sbase + 4u * (uint32_t)((OFF_A + i) * D));
                 apply_frag<CPL, MODE>(a, oc, acc.v, wv, av, (size_t)(ki & a.lmask) * D + col);
               }
             }
@@ -499,16 +511,16 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
     }
   }
   cp_async_wait<0>();
-  if (open) span_piece<CPL, MODE>(a, acc, begins ? 2 * gw + 1 : 2 * gw, open_pos, open_key, R, n);  // continues past the range
+  if (open && !broken) span_piece<CPL, MODE>(a, acc, begins ? 2 * gw + 1 : 2 * gw, open_pos, open_key, R, n);  // continues past the range
   if (MODE == 3) __threadfence_system();  // peer stores of this thread precede the GRADS flag
   if (a.signal_kind >= 0) grad_signal_last_warp(a, nwarps);
 }
 
 static int g_sms = 0;
 
-template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2>
+template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2, bool LO = false>
 static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
-  constexpr int NA = (MODE == 1) ? 3 : ((MODE == 0 || MODE == 4) ? 2 : 1);
+  constexpr int NA = ((MODE == 1) ? 3 : ((MODE == 0 || MODE == 4) ? 2 : 1)) + (LO ? 1 : 0);
   const size_t per_warp = (size_t)NS * ((size_t)NA * T * a.dim + (MODE == 4 ? T : 0)) * sizeof(float);
   int wpc = (int)(110 * 1024 / per_warp);  // warps per CTA: ~110 KB of stages, 2 CTAs per SM
   if (wpc > 8) wpc = 8;
@@ -520,36 +532,40 @@ static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
   if (dev < 0 || dev >= EMB_MAX_DEVICES) return cudaErrorInvalidDevice;
   if (attr[dev] < smem) {
     cudaError_t e =
-        cudaFuncSetAttribute(k_grad<CPL, T, NS, MEAN, MODE, DC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr[dev] = smem;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grad<CPL, T, NS, MEAN, MODE, DC, MINB>, wpc * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO>, wpc * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)g_sms * per_sm;
   const int64_t max_blocks = ((a.n + 4 * T - 1) / (4 * T) + wpc - 1) / wpc;  // >= 4 tiles per warp
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  k_grad<CPL, T, NS, MEAN, MODE, DC, MINB><<<(unsigned)blocks, wpc * 32, smem, st>>>(a);
+  k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO><<<(unsigned)blocks, wpc * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 template <int CPL, int T, int DC>
 static cudaError_t launch_grad_d(const GradArgs &a, cudaStream_t st) {
   const bool mean = a.blen != nullptr;
-  const int mode = a.sink_mode == 2 ? 3 : (a.sink_mode == 1 ? 2 : (a.opt == 1 ? 1 : (a.opt == 2 ? 4 : 0)));
+  const int mode = a.sink_mode == 2 ? 3 : (a.opt == 1 ? 1 : (a.opt == 2 ? 4 : 0));
   if (mean) {
     if (mode == 0) return launch_grad_t<CPL, T, 2, true, 0, DC>(a, st);
     if (mode == 1) return launch_grad_t<CPL, T, 2, true, 1, DC>(a, st);
     if (mode == 4) return launch_grad_t<CPL, T, 2, true, 4, DC>(a, st);
-    if (mode == 2) return launch_grad_t<CPL, T, 2, true, 2, DC>(a, st);
     return launch_grad_t<CPL, T, 2, true, 3, DC>(a, st);
+  }
+  if (a.src_lo) {  // owner side at W > 1: double-float received partials
+    if (mode == 0) return launch_grad_t<CPL, T, 2, false, 0, DC, 2, true>(a, st);
+    if (mode == 1) return launch_grad_t<CPL, T, 2, false, 1, DC, 2, true>(a, st);
+    if (mode == 4) return launch_grad_t<CPL, T, 2, false, 4, DC, 2, true>(a, st);
+    return cudaErrorInvalidValue;
   }
   if (mode == 0) return launch_grad_t<CPL, T, 2, false, 0, DC>(a, st);
   if (mode == 1) return launch_grad_t<CPL, T, 2, false, 1, DC>(a, st);
   if (mode == 4) return launch_grad_t<CPL, T, 2, false, 4, DC>(a, st);
-  if (mode == 2) return launch_grad_t<CPL, T, 2, false, 2, DC>(a, st);
   return launch_grad_t<CPL, T, 2, false, 3, DC>(a, st);
 }
 

@@ -7,35 +7,25 @@ constexpr int EMB_MAX_DEVICES = 64;  // per-device launch-attribute caches
 
 namespace emb {
 
-// Sharding / key-space parameters (R7). The ROUTING KEY of a fused row g is
-//   W == 1 : rk = g
-//   W  > 1 : rk = owner(g) << lbits | local(g)
-// so sorting routing keys groups the unique keys by owner, ascending local id within an owner.
+// Sharding / key-space parameters (R7). Every sorted key is the FUSED row g = base[t] + id (< 2^32):
+//   owner(g) = g mod W, local(g) = g div W          (cyclic, the default)
+//   owner(g) = g div rows_per, local(g) = g mod rows_per   (block)
+// At W == 1 owner = 0 and local = g.
 struct KeySpace {
   int32_t world;
   int32_t rank;
   int32_t shard;       // 0 cyclic, 1 block
-  uint32_t lbits;      // bits of the local row id (W > 1)
-  uint64_t rows_per;   // block sharding: ceil(R_total / W)
-  uint32_t key_bits;   // bits the radix sort must look at (sentinel strictly above every valid key)
+  uint32_t rows_per;   // block sharding: ceil(R_total / W)
+  uint32_t key_bits;   // bits the general radix sort must look at (sentinel strictly above every valid key)
 };
 
-__host__ __device__ inline uint32_t route_key(uint64_t g, const KeySpace &ks) {
-  if (ks.world == 1) return (uint32_t)g;
-  uint64_t owner, local;
-  if (ks.shard == 0) {
-    owner = g % (uint64_t)ks.world;
-    local = g / (uint64_t)ks.world;
-  } else {
-    owner = g / ks.rows_per;
-    local = g % ks.rows_per;
-  }
-  return (uint32_t)((owner << ks.lbits) | local);
+__host__ __device__ __forceinline__ uint32_t owner_of_g(uint32_t g, const KeySpace &ks) {
+  if (ks.world == 1) return 0;
+  return ks.shard == 0 ? g % (uint32_t)ks.world : g / ks.rows_per;
 }
-__host__ __device__ inline uint64_t key_to_global(uint32_t rk, const KeySpace &ks) {
-  if (ks.world == 1) return rk;
-  uint64_t owner = rk >> ks.lbits, local = rk & ((1u << ks.lbits) - 1u);
-  return ks.shard == 0 ? local * (uint64_t)ks.world + owner : owner * ks.rows_per + local;
+__host__ __device__ __forceinline__ uint32_t local_of_g(uint32_t g, const KeySpace &ks) {
+  if (ks.world == 1) return g;
+  return ks.shard == 0 ? g / (uint32_t)ks.world : g % ks.rows_per;
 }
 
 // kernel ids for the per-kernel event profiler (order = emb_profile_name)
@@ -47,48 +37,76 @@ enum KernelId {
   KID_GRAD_APPLY,
   KID_UNIQUE,
   KID_ROUTE,
-  KID_OWNER_GATHER,
-  KID_GRAD_LOCAL,
-  KID_NCCL,
+  KID_PULL,
+  KID_GRAD_PUSH,
+  KID_SIGNAL,
   KID_INIT,
   KID_MERGE,
   KID_WAIT,
   KID_COUNT
 };
 
-// ---- world > 1 peer-memory exchange (p2p.cu) ------------------------------------------------------
+// ---- world > 1 exchange over peer memory (p2p.cu, route.cu) ----------------------------------------
+// Every rank owns fixed per-source regions of `cap` entries (cap = max over ranks of max_ids) in its
+// receive buffers, so a source writes its keys / gradients without first learning where the other
+// sources' runs end. Flags are per-(kind, source) epoch words raised in every peer; a wait requires
+// EXACTLY the expected epoch (a rank that fell behind times out instead of reading stale buffers).
 constexpr int P2P_MAXW = 16;  // == EMB_MAX_WORLD
-enum { P2P_COUNTS = 0, P2P_KEYS = 1, P2P_ROWS = 2, P2P_GRADS = 3, P2P_NKIND = 4 };
-struct RouteTable {               // device-resident, rebuilt every step from the count matrix
-  int64_t soff[P2P_MAXW + 1];     // my send buffer: start of owner d's keys
-  int64_t roff[P2P_MAXW + 1];     // my receive buffer: start of source s's run
-  int64_t dst_off[P2P_MAXW];      // where my keys / gradients start in owner d's receive buffer
-  int64_t src_off[P2P_MAXW];      // where my rows start in requester s's row buffer
-  int64_t recv_counts[P2P_MAXW];
-  int64_t n_recv, n_send;
-};
+enum { P2P_KEYS = 0, P2P_GRADS = 1, P2P_APPLIED = 2, P2P_NKIND = 3 };
+// xmat layout (int64): [parity][0][s] = keys received from source s, [parity][1][s] = input-error
+// bits of source s in this step (parity = epoch & 1: double-buffered, a fast peer may already write
+// step e+1 while this rank still reads step e)
+__host__ __device__ __forceinline__ int xmat_idx(uint64_t epoch, int which, int s) {
+  return (int)(epoch & 1u) * 2 * P2P_MAXW + which * P2P_MAXW + s;
+}
 struct P2PArgs {
   int32_t world, rank;
   uint64_t epoch;
-  uint64_t *flags;                 // own [P2P_NKIND][P2P_MAXW]
-  int64_t *xmat;                   // own [W][W]
-  RouteTable *rt;
-  uint32_t *done;                  // own [P2P_NKIND] finished-block counters (last block raises the flag)
-  int64_t *peer_xmat[P2P_MAXW];
+  int64_t cap;                          // entries per source region
+  uint64_t *flags;                      // own [P2P_NKIND][P2P_MAXW]
+  uint32_t *done;                       // own [P2P_NKIND] finished-block counters (last block raises)
+  int64_t *xmat;                        // own [2][2][P2P_MAXW]
   uint64_t *peer_flags[P2P_MAXW];
-  uint32_t *peer_recv_keys[P2P_MAXW];
-  float *peer_uniq_rows[P2P_MAXW];
-  float *peer_grecv[P2P_MAXW];
+  int64_t *peer_xmat[P2P_MAXW];
+  uint32_t *peer_recv_keys[P2P_MAXW];   // [2][W * cap] owner-local ids, region s = source s
+  float *peer_grecv[P2P_MAXW];          // [2][W * cap][D] merged per-key gradients (hi, then lo parts),
+                                        // region s = source s
+  const float *peer_w[P2P_MAXW];        // table shards (the requester pulls its remote rows)
 };
-cudaError_t launch_push_rows(const P2PArgs &a, const float *rows, int dim, int64_t cap, cudaStream_t st);
-cudaError_t launch_xcounts(const P2PArgs &a, const int64_t *send_counts, uint32_t *err, cudaStream_t st);
-// device helpers (p2p_dev.cuh): the producing kernels (push_keys, gather_push, grad MODE 3) raise
-// their exchange flag from their last block / warp
-cudaError_t launch_signal(const P2PArgs &a, int kind, cudaStream_t st);
-cudaError_t launch_wait(const P2PArgs &a, int kind, uint32_t *err, cudaStream_t st);
-cudaError_t launch_push_keys(const P2PArgs &a, const uint32_t *send_keys, int64_t cap, cudaStream_t st);
-cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t *recv_keys, int dim, int64_t cap,
-                               int64_t rows_local, uint32_t *err, cudaStream_t st);
+// wait (one thread, bounded) until every source raised `kind` with exactly `epoch`
+cudaError_t launch_wait(const P2PArgs &a, int kind, uint64_t epoch, uint32_t *err, cudaStream_t st);
+// raise `kind` in every peer (a producer with nothing to do); err_bits != 0 are first OR-ed into every
+// owner's error slot of this step (xmat[parity][1][rank]): the owners then skip the update
+cudaError_t launch_signal(const P2PArgs &a, int kind, uint32_t err_bits, cudaStream_t st);
+// requester: uniq_rows[o*cap + i] = peer_w[o][send_local[o*cap + i]] for every remote owner o and
+// i < scnt[o] (peer loads over NVLink)
+cudaError_t launch_pull(const P2PArgs &a, const int64_t *scnt, const uint32_t *send_local, float *uniq_rows,
+                        int dim, int64_t max_rows, cudaStream_t st);
+
+// A3+A4 fused (route.cu): over the sorted fused keys, per distinct key (segment head) its owner o and
+// its rank `sendpos` among this rank's distinct keys owned by o (ascending g); the head's local id is
+// stored straight into owner o's receive region; per sorted position outidx = sendpos; per
+// occurrence inv = o*cap + sendpos. The last block publishes the per-owner counts and this rank's
+// input-error bits into every owner's xmat and raises KEYS.
+struct RouteArgs {
+  const uint32_t *skey, *spay;
+  int64_t n;
+  KeySpace ks;
+  P2PArgs p2p;
+  uint32_t *outidx;       // [n]
+  uint32_t *inv;          // [max_ids] by occurrence
+  uint32_t *send_local;   // [W * cap]
+  int64_t *scnt;          // [P2P_MAXW] out
+  uint32_t *tot;          // [P2P_MAXW] zero on entry, left zero
+  uint64_t *status;       // [tiles][P2P_MAXW] look-back words (epoch-tagged: no per-launch memset)
+  uint32_t *counter;      // tile ticket, self-resetting
+  uint32_t *blk_done;     // finished-block counter, self-resetting
+  uint32_t tag;           // distinct per launch, never 0
+  uint32_t *err;          // device sticky error word
+  uint32_t extra_err;     // host-detected argument error bits of this call (published + made sticky)
+};
+size_t route_status_words(int64_t max_n);
+cudaError_t launch_route(const RouteArgs &a, cudaStream_t st);
 
 // ---- launchers (each returns cudaGetLastError()) ------------------------------------------------
 struct KeysArgs {
@@ -100,8 +118,7 @@ struct KeysArgs {
   const int32_t *slot_table;  // device [S]
   const uint64_t *base;       // device [T]
   const int64_t *rows;        // device [T]
-  KeySpace ks;
-  uint32_t *key;     // out [nnz] routing key or EMB_SENTINEL
+  uint32_t *key;     // out [nnz] fused key g = base[t] + id, or EMB_SENTINEL
   uint32_t *drow;    // out [nnz] output row index b*S+s of the occurrence's bag (row of Y and dY)
   int32_t *blen;     // out [B*S] bag length, indexed by output row b*S+s
   uint32_t *err;     // sticky device error word
@@ -125,30 +142,35 @@ cudaError_t radix_sort_pairs(const SortWorkspace &ws, const uint32_t *kin, const
                              cudaStream_t st, uint32_t **keys_out, uint32_t **vals_out, int *launches,
                              ProfHook prof, void *prof_ctx);
 
-// W == 1 forward: Y[b][s][:] = pool over bag of table rows, straight from the table.
+// forward pool: Y[b][s][:] = sum (mean) over the bag's rows. A row g owned by this rank is read from
+// the table shard at local(g); at W > 1 a row owned by another rank from the pulled rows at inv[j].
 struct PoolArgs {
-  // W == 1 ("direct"): ids != nullptr; the pool validates the CSR and ids itself, computes the row
-  // g = base[t] + id, and writes the per-occurrence dY row index (drow) and bag lengths (blen).
+  // direct mode (ids != nullptr, monotone slot -> table map): the pool validates the CSR and ids
+  // itself, computes g = base[t] + id, and writes the per-occurrence dY row index (drow) and bag
+  // lengths (blen). Key mode (general sort path): g from `key` (the key kernel did all that).
   const int64_t *ids;      // [nnz] (direct mode) or nullptr
   const int32_t *slot_table;
   const uint64_t *base;
   const int64_t *rows;
   uint32_t *drow;          // out (direct mode) [nnz]
   int32_t *blen;           // out (direct mode) [B*S] or nullptr
-  const uint32_t *key;     // [nnz] routing keys in CSR order (EMB_SENTINEL = skip), key mode
+  const uint32_t *key;     // [nnz] fused keys in CSR order (EMB_SENTINEL = skip), key mode
   const int64_t *offsets;  // [S*B+1]
   int64_t nnz;
   int32_t batch, num_slots, dim;
   int32_t mean;
-  const float *rows_src;   // table (W==1) or received unique rows (W>1)
-  int64_t nrows_src;       // rows in rows_src (bounds guard)
-  const uint32_t *row_idx; // nullptr: row = key (W==1); else row = row_idx[j] (inverse -> unique index)
+  KeySpace ks;
+  const float *rows_src;   // the table shard
+  int64_t nrows_src;       // rows_local (bounds guard)
+  const float *rows_remote;  // W > 1: pulled rows [W*cap][D]
+  int64_t nrows_remote;      // W * cap (bounds guard)
+  const uint32_t *row_idx; // W > 1: inv (occurrence -> o*cap + sendpos) for rows owned elsewhere
   float *out;
   uint32_t *err;           // device error word
   uint32_t *err_host;      // mapped pinned host word
   uint32_t *fin;           // [3] finish counters (pool blocks, other kernel's blocks, kernels) or nullptr:
                            // when set, the last of the fin_kernels concurrently running kernels (pool +
-                           // segsort at W = 1, pool + owner merge at W > 1) publishes err to err_host
+                           // segsort at W = 1) publishes err to err_host
   uint32_t fin_kernels;
 };
 cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st);
@@ -156,11 +178,11 @@ cudaError_t launch_publish_err(const uint32_t *err, uint32_t *err_host, cudaStre
 
 // backward: segment reduce over sorted (key, pay) + sink
 struct GradArgs {
-  const uint32_t *skey;    // [n] sorted routing keys (sentinel last)
-  const uint32_t *spay;    // [n] payload (occurrence index j, or receive slot)
-  int64_t n;
+  const uint32_t *skey;    // [n] sorted keys (EMB_SENTINEL = invalid, skipped anywhere)
+  const uint32_t *spay;    // [n] payload (occurrence index j, or receive position)
+  int64_t n;               // positions (upper bound when n_dev is set: sizes the grid)
   int32_t dim;
-  // contribution source: mode 0 = dY rows via bag_of/blen; mode 1 = rows of `src` at index spay
+  // contribution source: mode 0 = dY rows via drow/blen; mode 1 = rows of `src` at index spay
   int32_t src_mode;
   const float *dy;         // [B][S][D]
   const uint32_t *drow;    // [nnz] dY row index b*S+s per occurrence
@@ -168,27 +190,30 @@ struct GradArgs {
   const int32_t *blen;     // [B*S] bag length by dY row (mean) or nullptr
   int32_t batch, num_slots;
   const float *src;        // mode 1
-  // sink: mode 0 = optimizer apply on table rows (local row = key & lmask); mode 1 = write fp32 row
-  // to out_rows[useg[p]] (requester-side local grad); mode 2 = the same row stored straight into the
-  // owner's gradient buffer through peer memory (p2p exchange)
+  const float *src_lo;     // mode 1, W > 1 owner side: low parts of the received double-float partials
+  int64_t lo_stride;       // sink 2: floats from a hi row to its lo row in the owner's region
+  // sink: 0 = optimizer apply on table rows (row = key & lmask); 2 = the merged fp32 row stored
+  // straight into the owner's gradient region through peer memory (requester side at W > 1)
   int32_t sink_mode;
   const int64_t *n_dev;    // if set, the number of sorted positions is read from the device
   int32_t signal_kind;     // >= 0: the last warp to finish raises this p2p flag in every peer
   P2PArgs p2p;             // sink mode 2 / signal
+  KeySpace ks;             // sink mode 2: owner of the key
+  // skip the whole pass (still signalling) when (*err & skip_mask) != 0 or any abort_bits[s] != 0,
+  // s < W: a step with an input error on any rank updates nothing (errors)
+  uint32_t skip_mask;
+  const int64_t *abort_bits;
   uint32_t lmask;
   int32_t opt;             // 0 sgd 1 adagrad 2 row-wise adagrad (a: one float per row)
   double lr, eps;
   float *w, *a;
   int64_t nrows;           // rows of w/a (bounds guard)
   int64_t nsrc;            // rows of dy (S*B) or src (bounds guard)
-  int64_t nout;            // rows of out_rows (bounds guard)
+  int64_t nout;            // sink 2: entries of a region (cap, bounds guard)
   uint32_t *err;
-  const uint32_t *useg;    // unique index per sorted position (dedup of skey)
-  const uint32_t *ustart;  // segment starts [U+1] (ustart[U] = number of valid positions)
-  const uint32_t *u_count; // device U
-  float *out_rows;
+  const uint32_t *useg;    // sink 2: per sorted position, the key's rank in its owner's list (outidx)
   double *partials;        // [2 * max resident warps][D]
-  uint32_t *tickets;       // [>= U], zero on entry, left zero
+  uint32_t *tickets;       // [>= n], zero on entry, left zero
 };
 cudaError_t launch_grad(const GradArgs &a, cudaStream_t st);
 int64_t grad_max_warps(int dev);
@@ -216,12 +241,6 @@ cudaError_t launch_rows_gather(const float *src, const int64_t *rows, int64_t n,
 cudaError_t launch_rows_scatter(float *dst, const int64_t *rows, int64_t n, int32_t dim, const float *src,
                                 cudaStream_t st);
 
-// W > 1 helpers
-cudaError_t launch_owner_counts(const uint32_t *ukey, const uint32_t *u_count, int32_t world, uint32_t lbits,
-                                int64_t *send_counts, cudaStream_t st);
-cudaError_t launch_scatter_inverse(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, int64_t n,
-                                   uint32_t *inv, cudaStream_t st);
-
 // per-table stable sort (world == 1 fast path), see segsort.cu
 constexpr int64_t SEG_CAP = 16384;
 struct SegSortArgs {
@@ -230,6 +249,7 @@ struct SegSortArgs {
   int64_t nnz;
   int32_t batch;
   const int32_t *gslot;     // [G+1] slot boundaries of the table groups
+  int32_t ngroups;          // G
   const uint64_t *gbase;    // [G] first fused key of the group's table
   const uint32_t *grows;    // [G] rows of the group's table
   const uint32_t *gbits;    // [G] bits covering [0, rows] (rows = the invalid marker)
@@ -237,25 +257,16 @@ struct SegSortArgs {
   uint32_t *scratch_k, *scratch_a, *scratch_b;  // [nnz] global buffers for chunks above the smem cap
   uint32_t *run_k, *run_i;  // [nnz] sorted runs (local key, chunk-relative index)
   int32_t K;                // chunks (CTAs) per group
+  int32_t validate;         // check the CSR offsets + fill uncovered positions (W > 1; the pool does it at W = 1)
   uint32_t *err;
   uint32_t *err_host;       // with fin: see PoolArgs::fin
   uint32_t *fin;
 };
 cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st);
-cudaError_t launch_local_of_unique(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, uint32_t lmask,
-                                   uint32_t *out, cudaStream_t st);
-cudaError_t launch_partition(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, const KeySpace &ks,
-                             uint32_t *tcnt, uint32_t *send_keys, uint32_t *sp, int64_t *send_counts,
-                             cudaStream_t st);
-cudaError_t launch_outidx(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, const uint32_t *sp,
-                          int64_t n, uint32_t *outidx, uint32_t *inv, cudaStream_t st);
-cudaError_t launch_merge_tree(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t cap, uint32_t *ok0,
-                              uint32_t *op0, uint32_t *ok1, uint32_t *op1, uint32_t *err, cudaStream_t st,
-                              uint32_t *fin, uint32_t *err_host);
-cudaError_t launch_merge_runs(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t n, uint32_t *okey,
-                              uint32_t *opay, uint32_t *err, cudaStream_t st, uint32_t *fin = nullptr,
-                              uint32_t *err_host = nullptr);
-cudaError_t launch_owner_gather(const float *w, const uint32_t *local, int64_t n, int32_t dim, float *out,
-                                cudaStream_t st);
+// owner side: stable merge of the W received runs (source s's run at s*cap, length counts[s], each
+// sorted by local id) into (ok0, op0): keys and receive positions s*cap + i, ties in source-rank order
+// (ceil(log2 W) merge-path passes); writes the merged length to *n_merged
+cudaError_t launch_merge_tree(const uint32_t *rkeys, const int64_t *counts, int W, int64_t cap, uint32_t *ok0,
+                              uint32_t *op0, uint32_t *ok1, uint32_t *op1, int64_t *n_merged, cudaStream_t st);
 
 }  // namespace emb

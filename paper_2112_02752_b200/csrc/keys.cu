@@ -1,9 +1,9 @@
-// keys.cu — K1: CSR parse + validation + fused routing keys (readings R4, R5, R7).
+// keys.cu — K1: CSR parse + validation + fused keys g = base[t] + id (readings R4, R5).
 //
 // One warp per 32 consecutive bags. Lane l holds bag (b0+l)'s [start, end) and its table's base/rows.
 // The warp then walks the contiguous id range [start(b0), end(b0+31)) 32 ids at a time (coalesced
 // int64 loads); each id finds its bag by a 5-step shuffle binary search over the lanes' starts, so
-// skewed bag lengths cost no divergence. Outputs per occurrence j: routing key (or EMB_SENTINEL for an
+// skewed bag lengths cost no divergence. Outputs per occurrence j: fused key g (or EMB_SENTINEL for an
 // invalid id) and its output row index b*S+s (the row of Y / dY it pools into); per bag: its length
 // at that same row index.
 #include "common.cuh"
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) k_keys(KeysArgs a) {
       } else if (id < 0 || id >= rowsl) {
         bad |= EMB_DEVERR_RANGE;
       } else {
-        rk = route_key(basel + (uint64_t)id, a.ks);
+        rk = (uint32_t)(basel + (uint64_t)id);  // fused key g (< 2^32 - 1)
       }
       a.key[j] = rk;
       a.drow[j] = orowl;

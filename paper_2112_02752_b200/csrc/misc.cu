@@ -1,5 +1,5 @@
-// misc.cu — dedup compaction (A2), owner routing helpers (A3/A5), owner-side row gather (A6 at
-// W > 1), table init (R15) and row export/import kernels.
+// misc.cu — dedup compaction (A2; step statistics and emb_last_unique), table init (R15) and row
+// export/import kernels.
 #include "common.cuh"
 #include "internal.h"
 
@@ -104,75 +104,6 @@ __global__ void __launch_bounds__(UQ_THREADS) k_unique(const __grid_constant__ U
 cudaError_t launch_unique(const UniqueArgs &a, cudaStream_t st) {
   const int64_t tiles = a.n > 0 ? (a.n + UQ_TILE - 1) / UQ_TILE : 1;
   k_unique<<<(unsigned)tiles, UQ_THREADS, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------------------------------------
-// owner routing helpers (W > 1)
-__global__ void k_owner_counts(const uint32_t *ukey, const uint32_t *u_count, int32_t world, uint32_t lbits,
-                               int64_t *send_counts) {
-  const int d = threadIdx.x;
-  if (d >= world) return;
-  const int64_t U = *u_count;
-  auto lb = [&](uint64_t x) {
-    int64_t lo = 0, hi = U;
-    while (lo < hi) {
-      const int64_t m = (lo + hi) >> 1;
-      if ((uint64_t)ukey[m] < x) lo = m + 1; else hi = m;
-    }
-    return lo;
-  };
-  send_counts[d] = lb((uint64_t)(d + 1) << lbits) - lb((uint64_t)d << lbits);
-}
-cudaError_t launch_owner_counts(const uint32_t *ukey, const uint32_t *u_count, int32_t world, uint32_t lbits,
-                                int64_t *send_counts, cudaStream_t st) {
-  k_owner_counts<<<1, 32, 0, st>>>(ukey, u_count, world, lbits, send_counts);
-  return cudaGetLastError();
-}
-
-__global__ void k_scatter_inverse(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, int64_t n,
-                                  uint32_t *inv) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const uint32_t k = skey[p];
-  inv[spay[p]] = k != EMB_SENTINEL ? useg[p] : EMB_SENTINEL;
-}
-cudaError_t launch_scatter_inverse(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, int64_t n,
-                                   uint32_t *inv, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  k_scatter_inverse<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(skey, spay, useg, n, inv);
-  return cudaGetLastError();
-}
-
-__global__ void k_local_of_unique(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, uint32_t lmask,
-                                  uint32_t *out) {
-  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= cap || u >= (int64_t)*u_count) return;
-  out[u] = ukey[u] & lmask;
-}
-cudaError_t launch_local_of_unique(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, uint32_t lmask,
-                                   uint32_t *out, cudaStream_t st) {
-  if (cap <= 0) return cudaSuccess;
-  k_local_of_unique<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(ukey, u_count, cap, lmask, out);
-  return cudaGetLastError();
-}
-
-// owner-side gather: out[i][:] = w[local[i]][:] (float4 per thread, a row per D/4 threads)
-__global__ void k_owner_gather(const float4 *__restrict__ w, const uint32_t *__restrict__ local, int64_t n, int d4,
-                               float4 *__restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i = t / d4;
-  const int c = (int)(t - i * d4);
-  if (i >= n) return;
-  out[t] = ld_nc_f4(w + (size_t)local[i] * d4 + c);
-}
-cudaError_t launch_owner_gather(const float *w, const uint32_t *local, int64_t n, int32_t dim, float *out,
-                                cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  const int d4 = dim / 4;
-  const int64_t total = n * d4;
-  k_owner_gather<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(reinterpret_cast<const float4 *>(w), local, n,
-                                                                  d4, reinterpret_cast<float4 *>(out));
   return cudaGetLastError();
 }
 

@@ -14,23 +14,28 @@ __device__ __forceinline__ uint64_t ld_acq_sys_u64(const uint64_t *p) {
   return v;
 }
 
-// one thread: spin (bounded) until every peer raised flag `kind` for this epoch
-__device__ __forceinline__ void p2p_spin(const P2PArgs &a, int kind, uint32_t *err) {
+// one thread: spin (bounded) until every source raised flag `kind` with exactly `epoch`. Exact match:
+// under the step protocol a flag never runs more than the awaited step ahead, so a
+// value other than `epoch` means a rank skipped a collective call; the wait then times out and sets
+// EMB_DEVERR_TIMEOUT (sticky; the consumers skip their work) instead of reading stale buffers. After a
+// timeout, later waits return at once (the handles must be recreated).
+__device__ __forceinline__ void p2p_spin(const P2PArgs &a, int kind, uint64_t epoch, uint32_t *err) {
+  if (ld_cg_u32(err) & EMB_DEVERR_TIMEOUT) return;
   for (int s = 0; s < a.world; ++s) {
     const uint64_t *f = a.flags + kind * P2P_MAXW + s;
     uint64_t spins = 0;
-    while (ld_acq_sys_u64(f) < a.epoch) {
+    while (ld_acq_sys_u64(f) != epoch) {
       __nanosleep(64);
-      if (++spins > (1ull << 26)) {  // a peer never arrived: report instead of hanging the GPU
+      if (++spins > (1ull << 26)) {  // ~4 s: a peer never arrived; report instead of hanging the GPU
         atomicOr(err, EMB_DEVERR_TIMEOUT);
-        break;
+        return;
       }
     }
   }
   __threadfence_system();
 }
 
-// one thread: raise flag `kind` for this rank in every peer
+// one thread: raise flag `kind` for this rank in every peer (after this thread's fence)
 __device__ __forceinline__ void p2p_raise(const P2PArgs &a, int kind) {
   __threadfence_system();
   for (int p = 0; p < a.world; ++p) st_sys_u64(a.peer_flags[p] + kind * P2P_MAXW + a.rank, a.epoch);

@@ -27,31 +27,50 @@ namespace {
 constexpr int POOL_THREADS = 256;
 }  // namespace
 
-// row of occurrence j. Direct mode (per-table sort path): g = base[t] + id validated here (R4), the
-// occurrence's dY row index recorded for the backward, and at W > 1 the row taken from row_idx (the
-// received-row index of the occurrence). Key mode (general sort path): from the routing key.
+// row of occurrence j. Direct mode (per-table sort path): g = base[t] + id validated here (R4) and the
+// occurrence's dY row index recorded for the backward; key mode (general sort path): g from the key
+// kernel. A row this rank owns is read from the table shard at local(g); at W > 1 a row owned by
+// another rank from the pulled rows at inv[j] (returned with REMOTE_BIT set).
+constexpr uint32_t REMOTE_BIT = 0x80000000u;
+template <bool REMOTE>
 __device__ __forceinline__ uint32_t pool_row_of(const PoolArgs &a, int64_t j, uint32_t slot, uint32_t orow) {
-  uint32_t row = EMB_SENTINEL;
+  uint32_t g = EMB_SENTINEL;
   if (a.ids) {
     const int t = a.slot_table[slot];
     const int64_t id = a.ids[j];
-    if (id >= 0 && id < a.rows[t]) row = (uint32_t)(a.base[t] + (uint64_t)id);
+    if (id >= 0 && id < a.rows[t]) g = (uint32_t)(a.base[t] + (uint64_t)id);
     else atomicOr(a.err, EMB_DEVERR_RANGE);
-    if (row != EMB_SENTINEL && a.row_idx) row = a.row_idx[j];  // W > 1: index of the received row
     a.drow[j] = orow;
   } else {
-    const uint32_t k = a.key[j];
-    if (k != EMB_SENTINEL) row = a.row_idx ? a.row_idx[j] : k;
+    g = a.key[j];
   }
-  if (row != EMB_SENTINEL && (int64_t)row >= a.nrows_src) {
+  if (g == EMB_SENTINEL) return EMB_SENTINEL;
+  if (REMOTE && owner_of_g(g, a.ks) != (uint32_t)a.ks.rank) {
+    const uint32_t r = a.row_idx[j];
+    if ((int64_t)r >= a.nrows_remote) {
+      atomicOr(a.err, EMB_DEVERR_INTERNAL);
+      return EMB_SENTINEL;
+    }
+    return REMOTE_BIT | r;
+  }
+  const uint32_t row = REMOTE ? local_of_g(g, a.ks) : g;
+  if ((int64_t)row >= a.nrows_src) {
     atomicOr(a.err, EMB_DEVERR_INTERNAL);
-    row = EMB_SENTINEL;
+    return EMB_SENTINEL;
   }
   return row;
 }
+// address of a row returned by pool_row_of (EMB_SENTINEL / inactive lanes read row 0 of the shard:
+// unconditional loads, zeroed before use)
+template <bool REMOTE>
+__device__ __forceinline__ const float *pool_row_ptr(const PoolArgs &a, uint32_t ri, bool ok, int D, int col) {
+  if (!ok) return a.rows_src;
+  if (REMOTE && (ri & REMOTE_BIT)) return a.rows_remote + (size_t)(ri & ~REMOTE_BIT) * D + col;
+  return a.rows_src + (size_t)ri * D + col;
+}
 
 // general tile: flattened walk over the occurrences [lo, hi) of the tile's bags, fp64 in order
-template <int CPL>
+template <int CPL, bool REMOTE>
 __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, int64_t hi, int64_t my_end,
                                                uint32_t my_orow, uint32_t my_slot, int nbt) {
   constexpr int RCH = 32 / CPL;
@@ -94,7 +113,7 @@ __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, in
     const uint32_t sl = __shfl_sync(0xffffffffu, my_slot, l < 32 ? l : 31);
     const uint32_t orw = __shfl_sync(0xffffffffu, my_orow, l < 32 ? l : 31);
     const bool ok = (lane < RCH) && j < hi;
-    return ok ? pool_row_of(a, j, sl, orw) : EMB_SENTINEL;
+    return ok ? pool_row_of<REMOTE>(a, j, sl, orw) : EMB_SENTINEL;
   };
   // close leading empty bags
   while (cb < nbt && cend <= lo) flush();
@@ -108,7 +127,7 @@ __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, in
     for (int r = 0; r < RCH; ++r) {  // unconditional loads (see the single-id path in k_pool)
       const uint32_t ri = __shfl_sync(0xffffffffu, row, r);
       const bool ok = ri != EMB_SENTINEL && active;
-      v[r].load_nc(a.rows_src + (size_t)(ok ? ri : 0u) * D + (active ? col : 0));
+      v[r].load_nc(pool_row_ptr<REMOTE>(a, ri, ok, D, col));
     }
 #pragma unroll
     for (int r = 0; r < RCH; ++r) {
@@ -126,7 +145,7 @@ __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, in
   while (cb < nbt) flush();
 }
 
-template <int CPL, int RCH, int MINB>
+template <int CPL, int RCH, int MINB, bool REMOTE>
 __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_constant__ PoolArgs a) {
   // RCH rows per batch of the single-id path (RCH * CPL floats in flight per lane)
   const int lane = threadIdx.x & 31;
@@ -163,11 +182,11 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
     if (__any_sync(0xffffffffu, len > 1)) {
       const int64_t lo = __shfl_sync(0xffffffffu, off, 0);
       const int64_t hi = __shfl_sync(0xffffffffu, offn, nbt - 1);
-      pool_tile_general<CPL>(a, lo, hi, offn, orow, s, nbt);
+      pool_tile_general<CPL, REMOTE>(a, lo, hi, offn, orow, s, nbt);
       continue;
     }
     // single-id bags: copy the row (exact)
-    const uint32_t row = (len == 1) ? pool_row_of(a, off, s, orow) : EMB_SENTINEL;
+    const uint32_t row = (len == 1) ? pool_row_of<REMOTE>(a, off, s, orow) : EMB_SENTINEL;
 #pragma unroll
     for (int c0 = 0; c0 < 32; c0 += RCH) {
       if (c0 >= nbt) break;
@@ -179,7 +198,7 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
         // rows in groups of ~4 between stores instead of RCH in flight
         const uint32_t ri = __shfl_sync(0xffffffffu, row, c0 + r);
         const bool ok = ri != EMB_SENTINEL && active;
-        v[r].load_nc(a.rows_src + (size_t)(ok ? ri : 0u) * D + (active ? col : 0));
+        v[r].load_nc(pool_row_ptr<REMOTE>(a, ri, ok, D, col));
       }
 #pragma unroll
       for (int r = 0; r < RCH; ++r) {
@@ -201,7 +220,10 @@ static cudaError_t launch_pool_t(const PoolArgs &a, int64_t ntiles, cudaStream_t
   // one tile per warp (not persistent), so the concurrent side-stream sort CTAs get SMs as soon as
   // they are ready and the pool fills the rest
   const int64_t blocks = (ntiles * 32 + POOL_THREADS - 1) / POOL_THREADS;
-  k_pool<CPL, RCH, MINB><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
+  if (a.ks.world > 1)
+    k_pool<CPL, RCH, MINB, true><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
+  else
+    k_pool<CPL, RCH, MINB, false><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -218,20 +240,9 @@ cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st) {
   const int64_t nb = (int64_t)a.num_slots * a.batch;
   if (nb == 0) return cudaSuccess;
   const int64_t ntiles = (nb + 31) / 32;
-  static int var = -1;
-  if (var < 0) {
-    const char *v = getenv("EMB_POOL_VAR");  // experiment knob (D <= 64): rows in flight x register cap
-    var = v ? atoi(v) : 0;
-  }
-  if (a.dim <= 64) {
-    if (var == 1) return launch_pool_t<2, 32, 2>(a, ntiles, st);
-    if (var == 7) return launch_pool_t<2, 16, 2>(a, ntiles, st);
-    if (var == 2) return launch_pool_t<2, 16, 3>(a, ntiles, st);
-    if (var == 3) return launch_pool_t<2, 8, 4>(a, ntiles, st);
-    // all 32 rows of a tile in flight per lane (registers allow it now that the loads are
-    // unconditional): C2 step 136.6 -> 133.5 us against 16 rows
-    return launch_pool_t<2, 32, 3>(a, ntiles, st);
-  }
+  // D <= 64: all 32 rows of a tile in flight per lane (registers allow it because the loads are
+  // unconditional): C2 step 136.6 -> 133.5 us against 16 rows (round 1)
+  if (a.dim <= 64) return launch_pool_t<2, 32, 3>(a, ntiles, st);
   if (a.dim <= 128) return launch_pool_t<4, 8, 3>(a, ntiles, st);
   return launch_pool_t<8, 4, 3>(a, ntiles, st);
 }

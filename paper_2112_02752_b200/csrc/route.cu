@@ -1,233 +1,267 @@
-// route.cu — shard routing for world > 1 (SURVEY §8(a) A3/A5; readings R5-R7).
+// route.cu — shard routing for world > 1 (SURVEY §8(a) A3-A5; readings R5-R7).
 //
-//  * k_part_count / k_part_scatter: stable partition of the rank's sorted distinct keys by owner
-//    (cyclic: g mod W; block: g div rows_per). Tiles of 2048 keys: per-(tile, owner) counts, then each
-//    CTA scans the tiny count matrix itself for its global offsets and ranks its keys stably with
-//    ballots. Output: send buffer of local ids (owner-major, ascending g inside an owner), the send
-//    position of every distinct key, and the per-owner counts (X0 payload).
-//  * k_outidx: per sorted occurrence: send position of its key (the row it gets back, and the slot of
-//    its merged gradient in the X3 send buffer); inverse[occurrence] for the pool.
-//  * k_merge_pass: the owner receives W runs (one per source rank), each sorted by local id; a stable
-//    merge tree (ceil(log2 W) passes of pairwise merge-path merges, ties keep the lower source rank)
-//    replaces a full radix sort of the received keys. Per pass, a CTA owns TILE outputs of one merged
-//    run: one merge-path search for its two diagonals, the A / B windows staged in shared memory, then
-//    per-thread searches and sequential merges there. (v1, k_merge_runs: every item ranked by binary
-//    searches into the W-1 other runs — 60 / 106 us at W = 2 / 4, growing with W.)
+//  * k_route (A3 + A4 fused): one pass over the rank's sorted fused keys (segments = distinct keys).
+//    Tiles of 4096 positions, claimed in launch order through a ticket (forward progress for the
+//    look-back); a warp walks 8 rows of 32 consecutive positions. Per row, MATCH.ANY groups the lanes
+//    by owner and a ballot marks the segment heads, so each lane knows how many heads of its owner
+//    precede it in the row; per-warp and per-tile counts of heads per owner give the exclusive base
+//    (warp prefix in shared memory, tile prefix by a decoupled look-back over W counters, one lane per
+//    owner). A position's key then has rank `sendpos` among this rank's distinct keys of that owner
+//    (ascending g). Outputs: outidx per sorted position (the row of the merged gradient in the owner's
+//    region), inv per occurrence (the row the pull brings back), the head's local id into the owner's
+//    receive region (peer store) and into the local pull list. The last block publishes the per-owner
+//    counts and this rank's input-error bits into every owner's xmat and raises KEYS.
+//  * k_merge_pass (A5): the owner receives W runs (source s at region s*cap), each sorted by local id;
+//    a stable merge tree (ceil(log2 W) passes of pairwise merge-path merges, ties keep the lower
+//    source rank) gives the owner's merged order. Per pass a CTA owns TILE outputs of one merged run:
+//    two merge-path diagonals found by warp-parallel 32-ary searches (4 dependent L2 round trips
+//    instead of ~17 for a serial binary search), the A / B windows staged in shared memory, then
+//    per-thread searches and sequential merges there.
 #include "../../include/emb.h"
 #include "common.cuh"
 #include "internal.h"
+#include "p2p_dev.cuh"
 
 namespace emb {
 
 namespace {
-constexpr int PT_THREADS = 256;
-constexpr int PT_ITEMS = 8;
-constexpr int PT_TILE = PT_THREADS * PT_ITEMS;  // 2048
+constexpr int RT_THREADS = 512;
+constexpr int RT_WARPS = RT_THREADS / 32;
+constexpr int RT_ROWS = 8;                      // rows of 32 positions per warp
+constexpr int RT_TILE = RT_THREADS * RT_ROWS;   // 4096 positions per CTA
+constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_VAL = (1u << 30) - 1u;
 }  // namespace
 
-__device__ __forceinline__ uint32_t owner_of(uint32_t g, const KeySpace &ks) {
-  return ks.shard == 0 ? g % (uint32_t)ks.world : (uint32_t)(g / ks.rows_per);
-}
-__device__ __forceinline__ uint32_t local_of(uint32_t g, const KeySpace &ks) {
-  return ks.shard == 0 ? g / (uint32_t)ks.world : (uint32_t)(g % ks.rows_per);
+size_t route_status_words(int64_t max_n) { return (size_t)((max_n + RT_TILE - 1) / RT_TILE + 1) * P2P_MAXW; }
+
+__device__ __forceinline__ unsigned lanemask_le() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+  return m;
 }
 
-__global__ void __launch_bounds__(PT_THREADS) k_part_count(const uint32_t *__restrict__ ukey,
-                                                           const uint32_t *__restrict__ u_count, KeySpace ks,
-                                                           uint32_t *__restrict__ tcnt) {
-  __shared__ uint32_t c[EMB_MAX_WORLD];
-  const uint32_t U = *u_count;
-  const uint32_t t0 = blockIdx.x * PT_TILE;
-  if (threadIdx.x < EMB_MAX_WORLD) c[threadIdx.x] = 0;
-  __syncthreads();
-  if (t0 < U) {
-    for (uint32_t i = t0 + threadIdx.x; i < min(U, t0 + PT_TILE); i += PT_THREADS)
-      atomicAdd(&c[owner_of(ukey[i], ks)], 1u);
-  }
-  __syncthreads();
-  if (threadIdx.x < (unsigned)ks.world) tcnt[blockIdx.x * EMB_MAX_WORLD + threadIdx.x] = c[threadIdx.x];
-}
-
-__global__ void __launch_bounds__(PT_THREADS) k_part_scatter(const uint32_t *__restrict__ ukey,
-                                                             const uint32_t *__restrict__ u_count, KeySpace ks,
-                                                             const uint32_t *__restrict__ tcnt, int ntiles,
-                                                             uint32_t *__restrict__ send_keys,
-                                                             uint32_t *__restrict__ sp,
-                                                             int64_t *__restrict__ send_counts) {
-  __shared__ uint32_t base[EMB_MAX_WORLD];              // global start of (this tile, owner)
-  __shared__ uint32_t wcnt[PT_THREADS / 32][EMB_MAX_WORLD];
-  __shared__ uint32_t s_before[EMB_MAX_WORLD], s_total[EMB_MAX_WORLD];
+__global__ void __launch_bounds__(RT_THREADS) k_route(const __grid_constant__ RouteArgs a) {
+  __shared__ uint32_t s_tile, s_last;
+  __shared__ uint32_t wcnt[RT_WARPS][P2P_MAXW];  // per (warp, owner) head counts -> running bases
+  __shared__ uint32_t s_excl[P2P_MAXW];          // heads of each owner in earlier tiles
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int W = ks.world;
-  const uint32_t U = *u_count;
-  const int tile = blockIdx.x;
-  // per owner: totals over all tiles and the part before this tile; warp d sums column d of the
-  // (tile, owner) count matrix with coalesced loads and a warp reduction (not one thread per owner
-  // walking every tile: that serial loop was most of this kernel's time)
-  for (int d = w; d < W; d += PT_THREADS / 32) {
-    uint32_t tot = 0, bef = 0;
-    for (int t = lane; t < ntiles; t += 32) {
-      const uint32_t v = tcnt[t * EMB_MAX_WORLD + d];
-      tot += v;
-      bef += t < tile ? v : 0u;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      bef += __shfl_xor_sync(0xffffffffu, bef, o);
-    }
-    if (lane == 0) {
-      s_total[d] = tot;
-      s_before[d] = bef;
-    }
+  const int W = a.p2p.world;
+  const int64_t cap = a.p2p.cap;
+  if (tid == 0) {
+    s_tile = atomicAdd(a.counter, 1u);
+    if (s_tile == gridDim.x - 1) *a.counter = 0;  // last ticket: ready for the next launch
   }
+  if (tid < RT_WARPS * P2P_MAXW) (&wcnt[0][0])[tid] = 0;
   __syncthreads();
-  if (tid < W) {
-    uint32_t before_owner = 0;
-    for (int d = 0; d < tid; ++d) before_owner += s_total[d];
-    base[tid] = before_owner + s_before[tid];
-    if (tile == 0) send_counts[tid] = s_total[tid];
+  const int64_t tile = s_tile;
+  const int64_t w0 = tile * RT_TILE + (int64_t)w * 32 * RT_ROWS;
+  uint32_t key[RT_ROWS];
+#pragma unroll
+  for (int r = 0; r < RT_ROWS; ++r) {
+    const int64_t p = w0 + r * 32 + lane;
+    key[r] = p < a.n ? a.skey[p] : EMB_SENTINEL;
   }
-  const uint32_t t0 = tile * PT_TILE;
-  // per-warp counts over the warp's contiguous 256 keys
-  const uint32_t w0 = t0 + w * 32 * PT_ITEMS;
-  if (lane < EMB_MAX_WORLD) wcnt[w][lane] = 0;
-  __syncwarp();
-  for (int r = 0; r < PT_ITEMS; ++r) {
-    const uint32_t i = w0 + r * 32 + lane;
-    const bool v = i < U;
-    const uint32_t o = v ? owner_of(ukey[i], ks) : 0;
-    const uint32_t peers = __match_any_sync(0xffffffffu, v ? o : 0x100u + lane);
-    if (v && lane == __ffs(peers) - 1) wcnt[w][o] += __popc(peers);
+  const uint32_t k_before = (lane == 0 && w0 > 0 && w0 - 1 < a.n) ? a.skey[w0 - 1] : EMB_SENTINEL;
+  // head / owner of the lane's position in row r (warp-collective)
+  auto row_info = [&](int r, bool &valid, bool &head, uint32_t &o, uint32_t &peers, uint32_t &hb) {
+    uint32_t prev = __shfl_up_sync(0xffffffffu, key[r], 1);
+    const uint32_t prev_row_last = __shfl_sync(0xffffffffu, r > 0 ? key[r > 0 ? r - 1 : 0] : 0u, 31);
+    if (lane == 0) prev = r == 0 ? k_before : prev_row_last;
+    valid = key[r] != EMB_SENTINEL;
+    head = valid && key[r] != prev;
+    o = valid ? owner_of_g(key[r], a.ks) : 0u;
+    peers = __match_any_sync(0xffffffffu, valid ? o : 0x100u + lane);
+    hb = __ballot_sync(0xffffffffu, head);
+  };
+  // ---- pass 1: heads per owner for this warp
+#pragma unroll
+  for (int r = 0; r < RT_ROWS; ++r) {
+    bool valid, head;
+    uint32_t o, peers, hb;
+    row_info(r, valid, head, o, peers, hb);
+    if (valid && lane == __ffs(peers) - 1) wcnt[w][o] += __popc(peers & hb);
     __syncwarp();
   }
   __syncthreads();
-  if (tid < W) {  // exclusive prefix over warps, per owner, on top of the tile base
-    uint32_t run = base[tid];
-    for (int q = 0; q < PT_THREADS / 32; ++q) {
-      const uint32_t c = wcnt[q][tid];
-      wcnt[q][tid] = run;
+  // ---- per owner: exclusive prefix over the warps, tile aggregate, look-back over earlier tiles
+  if (tid < W) {
+    const int o = tid;
+    uint32_t run = 0;
+    for (int q = 0; q < RT_WARPS; ++q) {
+      const uint32_t c = wcnt[q][o];
+      wcnt[q][o] = run;
       run += c;
     }
+    const uint32_t agg = run;
+    const unsigned long long tag = (unsigned long long)a.tag << 32;
+    volatile unsigned long long *st = reinterpret_cast<volatile unsigned long long *>(a.status);
+    uint32_t excl = 0;
+    if (tile == 0) {
+      st[o] = tag | LB_INC | agg;
+    } else {
+      st[tile * P2P_MAXW + o] = tag | LB_AGG | agg;
+      int64_t look = tile - 1;
+      while (true) {
+        unsigned long long s;
+        do {
+          s = st[look * P2P_MAXW + o];
+        } while ((s >> 32) != a.tag || ((uint32_t)s & ~LB_VAL) == 0);
+        excl += (uint32_t)s & LB_VAL;
+        if ((uint32_t)s & LB_INC) break;
+        --look;
+      }
+      st[tile * P2P_MAXW + o] = tag | LB_INC | (excl + agg);
+    }
+    s_excl[o] = excl;
+    if (agg) atomicAdd(a.tot + o, agg);
   }
   __syncthreads();
-  for (int r = 0; r < PT_ITEMS; ++r) {
-    const uint32_t i = w0 + r * 32 + lane;
-    const bool v = i < U;
-    const uint32_t g = v ? ukey[i] : 0;
-    const uint32_t o = v ? owner_of(g, ks) : 0;
-    const uint32_t peers = __match_any_sync(0xffffffffu, v ? o : 0x100u + lane);
-    const int leader = v ? __ffs(peers) - 1 : lane;
-    uint32_t b = 0;
-    if (v && lane == leader) {
-      b = wcnt[w][o];
-      wcnt[w][o] = b + __popc(peers);
-    }
-    b = __shfl_sync(0xffffffffu, b, leader);
-    if (v) {
-      const uint32_t dst = b + __popc(peers & lanemask_lt());
-      send_keys[dst] = local_of(g, ks);
-      sp[i] = dst;
+  // ---- pass 2: ranks, outputs, peer stores of the heads' local ids
+  const int parity_off = (int)(a.p2p.epoch & 1u);
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < RT_ROWS; ++r) {
+    bool valid, head;
+    uint32_t o, peers, hb;
+    row_info(r, valid, head, o, peers, hb);
+    const int64_t p = w0 + r * 32 + lane;
+    const uint32_t same = peers & hb;
+    if (p < a.n) {
+      uint32_t sp = EMB_SENTINEL;
+      if (valid) {
+        const uint32_t incl = __popc(same & lanemask_le());
+        const int64_t pos = (int64_t)s_excl[o] + wcnt[w][o] + incl - 1;  // the segment head's rank
+        if (pos < 0 || pos >= cap) {
+          bad = true;
+        } else {
+          sp = (uint32_t)pos;
+          a.inv[a.spay[p]] = (uint32_t)(o * cap + pos);
+          if (head) {
+            const uint32_t lk = local_of_g(key[r], a.ks);
+            a.send_local[o * cap + pos] = lk;
+            a.p2p.peer_recv_keys[o][(int64_t)parity_off * W * cap + (int64_t)a.p2p.rank * cap + pos] = lk;
+          }
+        }
+      }
+      a.outidx[p] = sp;
     }
     __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wcnt[w][o] += __popc(same);
+    __syncwarp();
   }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err, EMB_DEVERR_INTERNAL);
+  // ---- the last block publishes the counts + error bits and raises KEYS
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(a.blk_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  if (tid == 0) *a.blk_done = 0;
+  __threadfence();
+  if (tid < W) {
+    const int o = tid;
+    const int64_t c = atomicExch(a.tot + o, 0u);
+    a.scnt[o] = c;
+    uint32_t eb = ld_cg_u32(a.err) & (EMB_DEVERR_RANGE | EMB_DEVERR_INVALID);
+    if (a.extra_err) {
+      eb |= a.extra_err;
+      if (o == 0) atomicOr(a.err, a.extra_err);
+    }
+    a.p2p.peer_xmat[o][xmat_idx(a.p2p.epoch, 0, a.p2p.rank)] = c;
+    a.p2p.peer_xmat[o][xmat_idx(a.p2p.epoch, 1, a.p2p.rank)] = eb;
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (tid == 0) p2p_raise(a.p2p, P2P_KEYS);
 }
 
-cudaError_t launch_partition(const uint32_t *ukey, const uint32_t *u_count, int64_t cap, const KeySpace &ks,
-                             uint32_t *tcnt, uint32_t *send_keys, uint32_t *sp, int64_t *send_counts,
-                             cudaStream_t st) {
-  // at least one tile: with no ids this step the per-owner send counts must still be written (zeros),
-  // or the exchange would announce the previous step's counts
-  const int ntiles = cap > 0 ? (int)((cap + PT_TILE - 1) / PT_TILE) : 1;
-  k_part_count<<<ntiles, PT_THREADS, 0, st>>>(ukey, u_count, ks, tcnt);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  k_part_scatter<<<ntiles, PT_THREADS, 0, st>>>(ukey, u_count, ks, tcnt, ntiles, send_keys, sp, send_counts);
+cudaError_t launch_route(const RouteArgs &a, cudaStream_t st) {
+  // at least one block: with no ids the per-owner counts must still be published (zeros) and KEYS raised
+  const int64_t tiles = a.n > 0 ? (a.n + RT_TILE - 1) / RT_TILE : 1;
+  k_route<<<(unsigned)tiles, RT_THREADS, 0, st>>>(a);
   return cudaGetLastError();
 }
 
-// per sorted occurrence p: outidx[p] = send position of its distinct key; inverse[occurrence] = same
-__global__ void k_outidx(const uint32_t *__restrict__ skey, const uint32_t *__restrict__ spay,
-                         const uint32_t *__restrict__ useg, const uint32_t *__restrict__ sp, int64_t n,
-                         uint32_t *__restrict__ outidx, uint32_t *__restrict__ inv) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const bool v = skey[p] != EMB_SENTINEL;
-  const uint32_t o = v ? sp[useg[p]] : EMB_SENTINEL;
-  outidx[p] = o;
-  inv[spay[p]] = o;
-}
-cudaError_t launch_outidx(const uint32_t *skey, const uint32_t *spay, const uint32_t *useg, const uint32_t *sp,
-                          int64_t n, uint32_t *outidx, uint32_t *inv, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  k_outidx<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(skey, spay, useg, sp, n, outidx, inv);
-  return cudaGetLastError();
-}
-
-// ---- merge tree (v2)
+// ---- merge tree
 namespace {
 constexpr int MP_THREADS = 256;
 constexpr int MP_ITEMS = 8;
 constexpr int MP_TILE = MP_THREADS * MP_ITEMS;  // outputs per CTA
 }  // namespace
 
-// number of A items among the first d outputs of the stable merge of A (first) and B
-__device__ __forceinline__ int64_t merge_path(const uint32_t *A, int64_t m, const uint32_t *B, int64_t n, int64_t d) {
+// number of A items among the first d outputs of the stable merge of A (first) and B: the first i in
+// [max(0, d-n), min(d, m)] with A[i] > B[d-1-i] (or the upper end). Warp-collective 32-ary search.
+__device__ int64_t merge_path_warp(const uint32_t *A, int64_t m, const uint32_t *B, int64_t n, int64_t d) {
+  const int lane = threadIdx.x & 31;
   int64_t lo = d > n ? d - n : 0, hi = d < m ? d : m;
   while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (A[mid] <= B[d - 1 - mid]) lo = mid + 1;
-    else hi = mid;
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t i = lo + (int64_t)lane * step;
+    const bool f = i < hi && A[i] > B[d - 1 - i];  // predicate "A[i] <= B[d-1-i]" is false at i
+    const uint32_t m_ = __ballot_sync(0xffffffffu, f);
+    if (m_ == 0) {
+      const int last = (int)((hi - 1 - lo) / step);  // last probed lane
+      lo = lo + (int64_t)last * step + 1;
+    } else {
+      const int fl = __ffs(m_) - 1;
+      const int64_t ifl = lo + (int64_t)fl * step;
+      if (fl == 0) return ifl;
+      hi = ifl;
+      lo = lo + (int64_t)(fl - 1) * step + 1;
+    }
   }
   return lo;
 }
 
-// pass r: output run j = stable merge of sources [2j*w, (2j+1)*w) (A) and [(2j+1)*w, (2j+2)*w) (B),
-// w = 2^r. ip == nullptr: payload = receive position (first pass).
+// pass with width w (= 2^r): input run q covers sources [q*w, (q+1)*w); pass 0 reads source q's region
+// at q*cap (payload = receive position q*cap + i), later passes the compact previous output at P[q*w].
+// Output run j = stable merge of input runs 2j (A) and 2j+1 (B), written compactly at P[2j*w].
 __global__ void __launch_bounds__(MP_THREADS) k_merge_pass(const uint32_t *__restrict__ ik,
                                                            const uint32_t *__restrict__ ip,
-                                                           const int64_t *__restrict__ recv_counts, int W, int w,
-                                                           uint32_t *__restrict__ ok, uint32_t *__restrict__ op,
-                                                           uint32_t *err, uint32_t *fin, uint32_t *err_host) {
-  __shared__ int64_t P[EMB_MAX_WORLD + 1];
+                                                           const int64_t *__restrict__ counts, int W, int64_t cap,
+                                                           int w, uint32_t *__restrict__ ok, uint32_t *__restrict__ op,
+                                                           int64_t *n_merged) {
+  __shared__ int64_t P[P2P_MAXW + 1];
   __shared__ uint32_t sk[MP_TILE], sp[MP_TILE];
-  __shared__ int64_t s_a0, s_am, s_b0, s_bn, s_i0, s_i1, s_d0, s_d1, s_out;
+  __shared__ int64_t s_i0, s_i1;
   const int tid = threadIdx.x;
   if (tid == 0) {
     P[0] = 0;
-    for (int r = 0; r < W; ++r) P[r + 1] = P[r] + recv_counts[r];
+    for (int r = 0; r < W; ++r) P[r + 1] = P[r] + counts[r];
+    if (n_merged && blockIdx.x == 0) *n_merged = P[W];
   }
   __syncthreads();
   const int nruns = (W + 2 * w - 1) / (2 * w);
-  // block -> (output run j, tile within the run)
-  int j = -1;
-  int64_t tile = blockIdx.x;
-  for (int q = 0; q < nruns; ++q) {
-    const int64_t len = P[min(W, (2 * q + 2) * w)] - P[min(W, 2 * q * w)];
-    const int64_t nt = (len + MP_TILE - 1) / MP_TILE;
-    if (tile < nt) {
-      j = q;
-      break;
+  // grid-stride over the (output run, tile) pairs of all runs
+  for (int64_t gt = blockIdx.x;; gt += gridDim.x) {
+    int j = -1;
+    int64_t tile = gt;
+    for (int q = 0; q < nruns; ++q) {
+      const int64_t len = P[min(W, (2 * q + 2) * w)] - P[min(W, 2 * q * w)];
+      const int64_t nt = (len + MP_TILE - 1) / MP_TILE;
+      if (tile < nt) {
+        j = q;
+        break;
+      }
+      tile -= nt;
     }
-    tile -= nt;
-  }
-  if (j >= 0) {
-    if (tid == 0) {
-      const int64_t a0 = P[min(W, 2 * j * w)], b0 = P[min(W, (2 * j + 1) * w)], e = P[min(W, (2 * j + 2) * w)];
-      const int64_t m = b0 - a0, n = e - b0;
-      const int64_t d0 = tile * MP_TILE, d1 = min(d0 + MP_TILE, m + n);
-      s_a0 = a0;
-      s_am = m;
-      s_b0 = b0;
-      s_bn = n;
-      s_d0 = d0;
-      s_d1 = d1;
-      s_i0 = merge_path(ik + a0, m, ik + b0, n, d0);
-      s_i1 = merge_path(ik + a0, m, ik + b0, n, d1);
-      s_out = a0 + d0;  // merged run j starts where its A run started
+    if (j < 0) return;  // block-uniform
+    const int qa = 2 * j, qb = 2 * j + 1;
+    const int64_t m = P[min(W, (qa + 1) * w)] - P[min(W, qa * w)];
+    const int64_t n = P[min(W, (qb + 1) * w)] - P[min(W, qb * w)];
+    const int64_t a0 = w == 1 ? (int64_t)qa * cap : P[min(W, qa * w)];
+    const int64_t b0 = w == 1 ? (int64_t)min(qb, W - 1) * cap : P[min(W, qb * w)];
+    const int64_t d0 = tile * MP_TILE, d1 = min(d0 + MP_TILE, m + n);
+    const int wid = tid >> 5;
+    if (wid == 0) {
+      const int64_t i0 = merge_path_warp(ik + a0, m, ik + b0, n, d0);
+      if ((tid & 31) == 0) s_i0 = i0;
+    } else if (wid == 1) {
+      const int64_t i1 = merge_path_warp(ik + a0, m, ik + b0, n, d1);
+      if ((tid & 31) == 0) s_i1 = i1;
     }
     __syncthreads();
-    const int64_t a0 = s_a0, b0 = s_b0, i0 = s_i0, i1 = s_i1, d0 = s_d0, d1 = s_d1;
+    const int64_t i0 = s_i0, i1 = s_i1;
     const int na = (int)(i1 - i0), nb = (int)((d1 - i1) - (d0 - i0));
     const int64_t bj0 = b0 + (d0 - i0);
     for (int q = tid; q < na; q += MP_THREADS) {
@@ -250,7 +284,7 @@ __global__ void __launch_bounds__(MP_THREADS) k_merge_pass(const uint32_t *__res
         else hi = mid;
       }
       int ia = lo, ib = dd - lo;
-      const int64_t o = s_out + dd;
+      const int64_t o = P[min(W, qa * w)] + d0 + dd;  // merged run j starts where its A run starts
       for (int q = 0; q < MP_ITEMS && dd + q < tot; ++q) {
         const bool takeA = ib >= nb || (ia < na && sk[ia] <= sk[na + ib]);
         const int src = takeA ? ia : na + ib;
@@ -260,81 +294,28 @@ __global__ void __launch_bounds__(MP_THREADS) k_merge_pass(const uint32_t *__res
         else ++ib;
       }
     }
-  }
-  if (fin) {  // last pass: the later of this merge and the pool publishes the error word
-    __syncthreads();
-    if (tid == 0) finish_publish(fin + 1, fin + 2, 2, err, err_host);
+    __syncthreads();  // the windows are refilled by the next tile
   }
 }
 
-cudaError_t launch_merge_tree(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t cap, uint32_t *ok0,
-                              uint32_t *op0, uint32_t *ok1, uint32_t *op1, uint32_t *err, cudaStream_t st,
-                              uint32_t *fin, uint32_t *err_host) {
+cudaError_t launch_merge_tree(const uint32_t *rkeys, const int64_t *counts, int W, int64_t cap, uint32_t *ok0,
+                              uint32_t *op0, uint32_t *ok1, uint32_t *op1, int64_t *n_merged, cudaStream_t st) {
   int passes = 0;
   while ((1 << passes) < W) ++passes;
-  const int64_t blocks = (cap + MP_TILE - 1) / MP_TILE + W;  // >= sum over runs of their tiles
+  int64_t blocks = (W * cap + MP_TILE - 1) / MP_TILE + W;  // >= sum over runs of their tiles
+  if (blocks > 148 * 4) blocks = 148 * 4;                      // (grid-stride beyond that)
   const uint32_t *ik = rkeys, *ip = nullptr;
   for (int r = 0; r < passes; ++r) {
     const bool to0 = ((passes - 1 - r) & 1) == 0;  // the last pass lands in (ok0, op0)
     uint32_t *ok = to0 ? ok0 : ok1, *op = to0 ? op0 : op1;
-    k_merge_pass<<<(unsigned)blocks, MP_THREADS, 0, st>>>(ik, ip, recv_counts, W, 1 << r, ok, op, err,
-                                                          r == passes - 1 ? fin : nullptr, err_host);
+    k_merge_pass<<<(unsigned)blocks, MP_THREADS, 0, st>>>(ik, ip, counts, W, cap, 1 << r, ok, op,
+                                                          r == 0 ? n_merged : nullptr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     ik = ok;
     ip = op;
   }
   return cudaSuccess;
-}
-
-// owner side (v1, kept for the NCCL exchange path): stable W-way merge by ranking
-__global__ void k_merge_runs(const uint32_t *__restrict__ rkeys, const int64_t *__restrict__ recv_counts, int W,
-                             int64_t cap, uint32_t *__restrict__ okey, uint32_t *__restrict__ opay,
-                             uint32_t *err, uint32_t *fin, uint32_t *err_host) {
-  __shared__ int64_t start[EMB_MAX_WORLD + 1];
-  if (threadIdx.x == 0) {
-    start[0] = 0;
-    for (int r = 0; r < W; ++r) start[r + 1] = start[r] + recv_counts[r];
-  }
-  __syncthreads();
-  const int64_t n = start[W];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n && i < cap;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int r = 0;
-    while (r + 1 < W && i >= start[r + 1]) ++r;
-    const uint32_t k = rkeys[i];
-    int64_t pos = i - start[r];
-    for (int q = 0; q < W; ++q) {
-      if (q == r) continue;
-      int64_t lo = start[q], len = start[q + 1] - start[q];
-      while (len > 0) {  // count of run q's keys <= k (q < r) or < k (q > r)
-        const int64_t half = len >> 1;
-        const uint32_t x = rkeys[lo + half];
-        const bool before = (q < r) ? (x <= k) : (x < k);
-        lo = before ? lo + half + 1 : lo;
-        len = before ? len - half - 1 : half;
-      }
-      pos += lo - start[q];
-    }
-    if (pos < 0 || pos >= n) {
-      atomicOr(err, EMB_DEVERR_INTERNAL);
-      continue;
-    }
-    okey[pos] = k;
-    opay[pos] = (uint32_t)i;
-  }
-  if (fin) {  // the later of this merge and the pool publishes the error word (PoolArgs::fin)
-    __syncthreads();
-    if (threadIdx.x == 0) finish_publish(fin + 1, fin + 2, 2, err, err_host);
-  }
-}
-cudaError_t launch_merge_runs(const uint32_t *rkeys, const int64_t *recv_counts, int W, int64_t n, uint32_t *okey,
-                              uint32_t *opay, uint32_t *err, cudaStream_t st, uint32_t *fin, uint32_t *err_host) {
-  if (n <= 0) return cudaSuccess;
-  const int64_t blocks = (n + 255) / 256;
-  k_merge_runs<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(rkeys, recv_counts, W, n, okey, opay, err,
-                                                                          fin, err_host);
-  return cudaGetLastError();
 }
 
 }  // namespace emb

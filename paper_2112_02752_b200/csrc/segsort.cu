@@ -72,6 +72,31 @@ __device__ __forceinline__ void segsort_range_body(const SegSortArgs &a) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int K = a.K;
   const int g = blockIdx.x / K, bkt = blockIdx.x % K;
+  // CSR validation (R4; before any early return; W > 1 only -- at W = 1 the concurrent pool validates):
+  // CTA (g, bkt) checks the bkt-th 1/K slice of its group's bags, so every input error is known before
+  // the route publishes it. CTA (0, 0) also checks both ends and marks sorted positions no group covers
+  // (only with broken offsets) as invalid, so nothing stale from an earlier step is ever routed.
+  if (a.validate) {
+    const int64_t B = a.batch;
+    const int64_t nb_all = (int64_t)a.gslot[a.ngroups] * B;
+    const int64_t b_lo = (int64_t)a.gslot[g] * B, b_hi = (int64_t)a.gslot[g + 1] * B;
+    const int64_t per = (b_hi - b_lo + K - 1) / K;
+    const int64_t s0 = b_lo + per * bkt, s1 = min(b_hi, s0 + per);
+    bool bad = false;
+    for (int64_t i = s0 + tid; i < s1; i += SS_THREADS) {
+      const int64_t o0 = a.offsets[i], o1 = a.offsets[i + 1];
+      bad |= o0 < 0 || o1 < o0 || o1 > a.nnz;
+    }
+    if (blockIdx.x == 0) {
+      const int64_t first = a.offsets[0], last = a.offsets[nb_all];
+      if (tid == 0) bad |= first != 0 || last != a.nnz;
+      const int64_t f = first < 0 ? 0 : (first > a.nnz ? a.nnz : first);
+      int64_t l = last < f ? f : (last > a.nnz ? a.nnz : last);
+      for (int64_t i = tid; i < f; i += SS_THREADS) a.skey[i] = EMB_SENTINEL;
+      for (int64_t i = l + tid; i < a.nnz; i += SS_THREADS) a.skey[i] = EMB_SENTINEL;
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(a.err, EMB_DEVERR_INVALID);
+  }
   int64_t glo, ghi;
   group_bounds(a, g, glo, ghi);
   const uint32_t ng = (uint32_t)(ghi - glo);
@@ -100,13 +125,19 @@ __device__ __forceinline__ void segsort_range_body(const SegSortArgs &a) {
   const uint32_t span = ((ng + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;
   const uint32_t s_lo = w * span, s_hi = min(ng, s_lo + span);
   uint32_t below = 0, mine = 0;
+  bool badid = false;
   for (uint32_t r0 = s_lo; r0 < s_hi; r0 += 32) {
     const uint32_t i = r0 + lane;
     uint32_t bb = 0xFFFFFFFFu;
-    if (i < s_hi) bb = bucket_of(key_at(i));
+    if (i < s_hi) {
+      const uint32_t lk = key_at(i);
+      badid |= lk == rows;
+      bb = bucket_of(lk);
+    }
     below += __popc(__ballot_sync(0xffffffffu, bb < (uint32_t)bkt));
     mine += __popc(__ballot_sync(0xffffffffu, bb == (uint32_t)bkt));
   }
+  if (bkt == 0 && __any_sync(0xffffffffu, badid) && lane == 0) atomicOr(a.err, EMB_DEVERR_RANGE);  // (R4)
   if (lane == 0) {
     wbelow[w] = below;
     wmine[w] = mine;
@@ -235,7 +266,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_const
 size_t segsort_smem_bytes() { return (size_t)SEG_CHUNK_CAP * 16 + (size_t)SEG_CAP * 4; }
 
 cudaError_t launch_segsort(const SegSortArgs &a, int32_t groups, cudaStream_t st) {
-  if (groups <= 0 || a.nnz <= 0) return cudaSuccess;
+  if (groups <= 0 || a.nnz <= 0 || a.batch <= 0) return cudaSuccess;
   static bool attr[EMB_MAX_DEVICES] = {};  // per device: the attribute is a per-context setting
   int dev = 0;
   cudaGetDevice(&dev);

@@ -27,8 +27,8 @@ SHARD = {"cyclic": 0, "block": 1}
 
 # every symbol include/emb.h declares (checked by tests/test_abi.py)
 EXPORTED = [
-    "emb_create", "emb_destroy", "emb_get_unique_id", "emb_lookup", "emb_lookup_prefetch", "emb_backward_update",
-    "emb_lookup_host",
+    "emb_create", "emb_create_group", "emb_destroy", "emb_get_unique_id", "emb_lookup", "emb_lookup_prefetch",
+    "emb_backward_update", "emb_lookup_group", "emb_backward_update_group", "emb_lookup_host",
     "emb_backward_update_host", "emb_read_rows", "emb_write_rows", "emb_last_step_info", "emb_last_unique",
     "emb_last_owner_unique", "emb_rows_local", "emb_profile_enable", "emb_profile_reset", "emb_profile_read",
     "emb_profile_name", "emb_clear_error", "emb_last_error",
@@ -78,6 +78,12 @@ def lib() -> ctypes.CDLL:
     L = ctypes.CDLL(LIB_PATH)
     vp, i32, i64, u64p, i64p = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p
     L.emb_create.argtypes = [ctypes.POINTER(EmbConfigC), ctypes.POINTER(vp)]
+    L.emb_create_group.argtypes = [ctypes.POINTER(EmbConfigC), i32, ctypes.POINTER(vp)]
+    L.emb_lookup_group.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(vp),
+                                   ctypes.POINTER(vp)]
+    L.emb_backward_update_group.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(vp), ctypes.c_double,
+                                            ctypes.POINTER(vp)]
     L.emb_destroy.argtypes = [vp]
     L.emb_get_unique_id.argtypes = [vp]
     L.emb_lookup.argtypes = [vp, vp, vp, i32, i64, vp, vp]
@@ -141,30 +147,39 @@ def get_unique_id() -> bytes:
     return buf.raw
 
 
+def _config(rows, dim, slot_table, pool, opt, eps, init_accum, seed, max_batch, max_ids, rank, world, nid, device,
+            shard):
+    return EmbConfigC(
+        num_tables=len(rows), rows=rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        dim=dim, num_slots=len(slot_table),
+        slot_table=slot_table.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+        pool=POOL[pool], opt=OPT[opt], eps=eps, init_accum=init_accum, init_seed=seed,
+        max_batch=max_batch, max_ids=max_ids, rank=rank, world=world,
+        nccl_id=ctypes.cast(nid, ctypes.c_void_p) if nid is not None else None,
+        device=device, shard=SHARD[shard])
+
+
 class EmbeddingLayer:
     """One rank's handle of the sparse embedding layer (include/emb.h emb_create)."""
 
     def __init__(self, rows: Sequence[int], dim: int, slot_table: Sequence[int], *, pool: str = "sum",
                  opt: str = "adagrad", eps: float = 1e-6, init_accum: float = 0.0, seed: int = 2112,
                  max_batch: int, max_ids: int, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-                 device: int = 0, shard: str = "cyclic"):
+                 device: int = 0, shard: str = "cyclic", _handle=None):
         L = lib()
         self._rows = np.ascontiguousarray(rows, dtype=np.int64)
         self._slots = np.ascontiguousarray(slot_table, dtype=np.int32)
         self._nid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        cfg = EmbConfigC(
-            num_tables=len(self._rows), rows=self._rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-            dim=dim, num_slots=len(self._slots),
-            slot_table=self._slots.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-            pool=POOL[pool], opt=OPT[opt], eps=eps, init_accum=init_accum, init_seed=seed,
-            max_batch=max_batch, max_ids=max_ids, rank=rank, world=world,
-            nccl_id=ctypes.cast(self._nid, ctypes.c_void_p) if self._nid is not None else None,
-            device=device, shard=SHARD[shard])
-        h = ctypes.c_void_p()
-        st = L.emb_create(ctypes.byref(cfg), ctypes.byref(h))
-        if st != EMB_OK:
-            raise EmbError(st, L.emb_last_error(None).decode())
-        self.h = h
+        if _handle is None:
+            cfg = _config(self._rows, dim, self._slots, pool, opt, eps, init_accum, seed, max_batch, max_ids, rank,
+                          world, self._nid, device, shard)
+            h = ctypes.c_void_p()
+            st = L.emb_create(ctypes.byref(cfg), ctypes.byref(h))
+            if st != EMB_OK:
+                raise EmbError(st, L.emb_last_error(None).decode())
+            self.h = h
+        else:
+            self.h = _handle
         self.dim, self.num_slots, self.device, self.world, self.rank = dim, len(self._slots), device, world, rank
         self.rows = tuple(int(r) for r in self._rows)
         self.slot_table = tuple(int(s) for s in self._slots)
@@ -273,3 +288,59 @@ class EmbeddingLayer:
 
     def last_error(self) -> str:
         return lib().emb_last_error(self.h).decode()
+
+
+class EmbeddingGroup:
+    """All `world` ranks of a row-sharded layer in this process (include/emb.h emb_create_group): rank r
+    on devices[r] (devices may repeat: several ranks emulated on one GPU). Step with lookup() /
+    backward_update() over per-rank argument lists; .layers[r] gives the per-rank helpers (read_rows,
+    step_info, last_unique, ...)."""
+
+    def __init__(self, rows: Sequence[int], dim: int, slot_table: Sequence[int], *, world: int,
+                 devices: Optional[Sequence[int]] = None, pool: str = "sum", opt: str = "adagrad", eps: float = 1e-6,
+                 init_accum: float = 0.0, seed: int = 2112, max_batch: int, max_ids, shard: str = "cyclic"):
+        L = lib()
+        devices = list(devices) if devices is not None else [0] * world
+        max_ids = list(max_ids) if isinstance(max_ids, (list, tuple)) else [int(max_ids)] * world
+        self._rows = np.ascontiguousarray(rows, dtype=np.int64)
+        self._slots = np.ascontiguousarray(slot_table, dtype=np.int32)
+        cfgs = (EmbConfigC * world)(*[
+            _config(self._rows, dim, self._slots, pool, opt, eps, init_accum, seed, max_batch, max_ids[r], r, world,
+                    None, devices[r], shard) for r in range(world)])
+        hs = (ctypes.c_void_p * world)()
+        st = L.emb_create_group(cfgs, world, hs)
+        if st != EMB_OK:
+            raise EmbError(st, L.emb_last_error(None).decode())
+        self._hs = hs
+        self.world, self.devices = world, devices
+        self.layers = [EmbeddingLayer(rows, dim, slot_table, pool=pool, opt=opt, eps=eps, init_accum=init_accum,
+                                      seed=seed, max_batch=max_batch, max_ids=max_ids[r], rank=r, world=world,
+                                      device=devices[r], shard=shard, _handle=ctypes.c_void_p(hs[r]))
+                       for r in range(world)]
+
+    def _streams(self, streams):
+        if streams is None:
+            streams = [None] * self.world
+        return (ctypes.c_void_p * self.world)(*[_stream(s, d) for s, d in zip(streams, self.devices)])
+
+    def lookup(self, ids, offsets, batch, nnz, out, streams=None):
+        W = self.world
+        st = lib().emb_lookup_group(self._hs, W, (ctypes.c_void_p * W)(*[_ptr(x) for x in ids]),
+                                    (ctypes.c_void_p * W)(*[_ptr(x) for x in offsets]),
+                                    (ctypes.c_int32 * W)(*[int(b) for b in batch]),
+                                    (ctypes.c_int64 * W)(*[int(n) for n in nnz]),
+                                    (ctypes.c_void_p * W)(*[_ptr(x) for x in out]), self._streams(streams))
+        if st != EMB_OK:
+            raise EmbError(st, "emb_lookup_group: " + "; ".join(l.last_error() for l in self.layers))
+
+    def backward_update(self, d_out, lr: float, streams=None):
+        W = self.world
+        st = lib().emb_backward_update_group(self._hs, W, (ctypes.c_void_p * W)(*[_ptr(x) for x in d_out]),
+                                             float(lr), self._streams(streams))
+        if st != EMB_OK:
+            raise EmbError(st, "emb_backward_update_group: " + "; ".join(l.last_error() for l in self.layers))
+
+    def close(self):
+        for l in getattr(self, "layers", []):
+            l.close()
+        self.layers = []

@@ -27,3 +27,11 @@ class DeviceBatch:
         self.offsets = torch.from_numpy(np.ascontiguousarray(bt.offsets)).to(dev)
         self.dy = torch.from_numpy(np.ascontiguousarray(bt.dy)).to(dev) if bt.dy is not None else None
         self.out = torch.empty((bt.batch, num_slots, dim), dtype=torch.float32, device=dev)
+
+
+def make_group(wl, *, world: int, max_batch: int, max_ids, devices=None, shard: str = "cyclic"):
+    """All `world` ranks of a row-sharded layer in this process (emb_create_group)."""
+    from .emb import EmbeddingGroup
+    return EmbeddingGroup(wl.rows, wl.dim, wl.slot_table, world=world, devices=devices, pool=wl.pool, opt=wl.opt,
+                          eps=wl.eps, init_accum=wl.init_accum, seed=wl.seed, max_batch=max_batch, max_ids=max_ids,
+                          shard=shard)

@@ -1,5 +1,7 @@
-"""Multi-GPU parity (-m gpu, needs >= 2 GPUs): row-sharded layer over 2 GPUs with NCCL all-to-alls
-inside libemb vs the serial oracle (tests/mgpu_worker.py, one process per GPU via torchrun)."""
+"""Multi-GPU parity (-m gpu, needs >= 2 GPUs): the row-sharded layer with one process per GPU (libemb's
+peer-memory exchange between processes over CUDA IPC mappings) vs the serial oracle
+(tests/mgpu_worker.py via torchrun). The same exchange with all ranks in one process (any number of
+GPUs, including one) is tests/test_group_parity.py."""
 import os
 import socket
 import subprocess
@@ -28,22 +30,15 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("case,shard,exchange", [("c3", "cyclic", "p2p"), ("hot", "cyclic", "p2p"),
-                                                 ("c3", "block", "p2p"), ("c3rw", "cyclic", "p2p"),
-                                                 ("c3full", "cyclic", "p2p"), ("c3", "cyclic", "nccl"),
-                                                 ("gen", "cyclic", "p2p"), ("hot", "block", "nccl"),
-                                                 ("edge", "cyclic", "p2p"), ("edge", "block", "nccl")])
-def test_two_gpu_row_sharded_parity(case, shard, exchange):
-    """exchange: "p2p" = the peer-memory exchange kernels (default); "nccl" = the v1 grouped
-    send/recv exchange (EMB_EXCHANGE=nccl). Case "gen" has a non-monotone slot -> table map, which
-    takes the general sort path and the NCCL exchange whatever `exchange` says."""
+@pytest.mark.parametrize("case,shard", [("c3", "cyclic"), ("hot", "cyclic"), ("c3", "block"), ("c3rw", "cyclic"),
+                                        ("c3full", "cyclic"), ("gen", "cyclic"), ("hot", "block"),
+                                        ("edge", "cyclic"), ("edge", "block")])
+def test_two_gpu_row_sharded_parity(case, shard):
     if _ngpu() < 2:
-        pytest.skip("needs 2 GPUs")
+        pytest.skip("needs 2 GPUs (the one-GPU equivalent is tests/test_group_parity.py)")
     from paper_2112_02752_b200 import build
     build.build()
     env = dict(os.environ, EMB_MGPU_CASE=case, EMB_MGPU_SHARD=shard)
-    if exchange == "nccl":
-        env["EMB_EXCHANGE"] = "nccl"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tests", "mgpu_worker.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
