@@ -5,10 +5,11 @@ update) through the C-ABI library, on synthetic BASELINE.json workloads.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N = 1 : workload C2 (BJ:8, the config BASELINE's metric is quoted on): 26 slots x 10M rows/table,
-        D = 64, B = 16,384, Zipf(1.05) ids, element-wise Adagrad, sum pooling.
+        D = 64, B = 16,384, Zipf(1.05) ids, element-wise Adagrad, sum pooling. The line also carries
+        `c3_w1`: C3 on this one GPU, the same-config denominator of the N > 1 (weak-scaling) lines.
 N > 1 : workload C3 (BJ:9) row-sharded (cyclic) over N GPUs, B = 16,384 per GPU (weak scaling),
-        launched with torchrun (one process per GPU; libemb exchanges ids / rows / gradients over
-        NVLink peer memory with its own kernels).
+        launched with torchrun (one process per GPU; libemb exchanges keys / rows / gradients over
+        NVLink peer memory with its own kernels); the line carries `nvlink` (bytes and link fraction).
 --impl reference: the CPU oracle (oracle/, NumPy fp64) timed on the host cores on a bounded sample of
         the same workload (rank 0 only).
 
@@ -44,11 +45,12 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def _traffic(kernel: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed ncu capture, or None."""
+def _traffic(kernel: str, opt: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` (for this optimizer) from the
+    committed ncu capture, or None."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        return d[kernel]["traffic_bytes"]
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
+        return d[f"{kernel}/{opt}"]["traffic_bytes"]
     except Exception:
         return None
 
@@ -89,20 +91,31 @@ def kernel_bytes(name, wl, N, SB, U, W, U_l=None):
     this GPU (U_o), U_l = distinct keys this GPU requested."""
     D = wl.dim
     U_l = U if U_l is None else U_l
-    if name == "grad_local":
-        # W > 1 requester merge: dY row + sorted key/payload/dY-row index per occurrence, one merged fp32
-        # row per requested key written (to its owner, (W-1)/W of them over NVLink)
-        return 4 * D * N + 12 * N + 4 * D * U_l
-    if name == "owner_gather":
-        # received key + table row read + row written to the requester, per received key (~U_l per rank)
-        return 4 * U_l + 8 * D * U_l
+    rem = U_l * (W - 1) / W  # requested keys owned by other ranks (uniform owners)
+    if name == "grad_push":
+        # W > 1 requester merge: dY row + sorted key/payload/dY-row index + rank per occurrence, one merged
+        # double-float row (hi + lo) per requested key written (to its owner, (W-1)/W of them over NVLink)
+        return 4 * D * N + 16 * N + 8 * D * U_l
+    if name == "gather_push":
+        # per key another rank requested from this owner: its local id + the table row read + the row
+        # stored into the requester's region (over NVLink)
+        return rem * (4 + 8 * D)
     if name == "grad_apply":
-        # dY row per occurrence + sorted key/payload/bag index per occurrence + state RMW per touched row
-        return 4 * D * N + 12 * N + state_bytes(wl, U)
+        if W == 1:  # dY row per occurrence + sorted key/payload/bag index per occurrence + state RMW per row
+            return 4 * D * N + 12 * N + state_bytes(wl, U)
+        # owner: merged key + receive position + hi/lo rows per received key (~U_l per rank) + state RMW
+        return U_l * (8 + 8 * D) + state_bytes(wl, U)
     if name == "pool":
-        # offsets + routing keys + one table row per distinct key + Y write
-        return 8 * (SB + 1) + 4 * N + 4 * D * U + 4 * D * SB
+        # offsets + ids + one row per distinct key + Y write
+        return 8 * (SB + 1) + 8 * N + 4 * D * U + 4 * D * SB
     return None
+
+
+def nvlink_bytes(wl, U_l, W):
+    """Bytes one GPU sends (= receives, symmetric) over NVLink per step (SURVEY §8(d) with the
+    double-float gradient, reading R11''): keys (4 B) + pulled rows (4D) + gradient hi/lo (8D) per
+    remote distinct key."""
+    return 0 if W == 1 else (W - 1) / W * U_l * (4 + 4 * wl.dim + 8 * wl.dim)
 
 
 # ------------------------------------------------------------------------------ clocks sampler
@@ -204,6 +217,9 @@ def main():
     ap.add_argument("--workload", default=None, help="override (C1..C5) for experiments")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3-at-1-GPU weak-scaling record (N = 1)")
+    ap.add_argument("--profile-steps", type=int, default=24,
+                    help="untimed steps with per-kernel events after the headline loop")
     ap.add_argument("--opt", default=None, choices=["sgd", "adagrad", "rowwise_adagrad"],
                     help="override the optimizer (experiments; BJ:8 is element-wise Adagrad)")
     args = ap.parse_args()
@@ -245,13 +261,69 @@ def main():
     if n > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_2112_02752_b200 import emb as E
-    from paper_2112_02752_b200.harness import DeviceBatch, make_layer
 
     nccl_id = None
     if n > 1:
         obj = [E.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+
+    def barrier():
+        if n > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    res = run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps=args.e2e_steps,
+                       profile_steps=args.profile_steps)
+    # weak-scaling denominator (N = 1 only): C3 -- the workload the N > 1 lines run -- on this one GPU
+    c3_w1 = None
+    if n == 1 and not args.workload and not args.no_c3:
+        r3 = run_workload(synthgen.WORKLOADS["C3"], args, 1, 0, local_rank, None, barrier, e2e_steps=0,
+                          profile_steps=0)
+        c3_w1 = {"workload": describe(synthgen.WORKLOADS["C3"], 1), "value": r3["value"], "unit": "samples/s",
+                 "ms_per_step": r3["ms_per_step"], "step_roofline": r3["step_roofline"],
+                 "note": "same config as the N>1 lines (C3, B=16,384 per GPU): the weak-scaling denominator"}
+
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu:  # the CPU baseline is an N = 1 figure
+        sps, lps, sample = oracle_time(wl, budget_s=args.cpu_budget)
+        thr, pool = cpu_threads()
+        cpu = {"value": sps, "unit": "samples/s", "cores": thr, "kind": "oracle",
+               "sample": sample + f"; host has {os.cpu_count()} cores, NumPy primitives single-threaded",
+               "lookups_per_s": lps}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": "samples/s", "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (fp64 accumulation)", "data": "synthetic",
+            "config": res["config"],
+            "lookups_per_s": res["lookups_per_s"],
+            "fwd_ms": res["fwd_ms"],
+            "step_roofline": res["step_roofline"],
+            "roofline": res["roofline"],
+            "nvlink": res["nvlink"],
+            "kernels": res["kernels"],
+            "cpu_baseline": cpu,
+            "e2e": res["e2e"],
+            "c3_w1": c3_w1,
+            "gpu_launches": res["gpu_launches"],
+            "clocks": res["clocks"],
+        }
+        print(json.dumps(line), flush=True)
+    if n > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, profile_steps):
+    """Time `args.steps` fwd+bwd+update steps of `wl` (inputs resident in HBM) on this rank; returns the
+    fields of the JSON line. The headline loop carries no per-kernel events; a separate profiled loop of
+    `profile_steps` steps (libemb's event profiler, every kernel on the stream it runs on) gives the
+    per-kernel breakdown, the forward time and the dominant kernel's roofline."""
+    import torch
+    import torch.distributed as dist
+    from paper_2112_02752_b200.harness import DeviceBatch, make_layer
 
     # stage a pool of distinct batches in HBM (inputs resident before the timed region)
     host_batches = [synthgen.make_batch(wl, rank=rank, step=i) for i in range(POOL_BATCHES)]
@@ -260,27 +332,22 @@ def main():
     layer = make_layer(wl, max_batch=wl.batch, max_ids=max_nnz, world=n, rank=rank, nccl_id=nccl_id,
                        device=local_rank)
     stream = torch.cuda.current_stream()
-
     use_prefetch = bool(os.environ.get("EMB_BENCH_PREFETCH"))  # experiment (measured slower)
-
-    def prefetch_next(i):
-        # pipelining (W = 1): the dedup sort of step i+1 enqueued before step i's backward
-        # (emb_lookup_prefetch). Off by default: the persistent gradient kernel holds the shared memory
-        # the sort needs, so the sort waits for it and the step got slower (140 -> 146 us)
-        if use_prefetch:
-            nx = dev_batches[(i + 1) % POOL_BATCHES]
-            layer.lookup_prefetch(nx.ids, nx.offsets, nx.batch, nx.nnz, stream)
 
     def step(i):
         db = dev_batches[i % POOL_BATCHES]
         layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
-        prefetch_next(i)
+        if use_prefetch:  # the dedup sort of step i+1 enqueued before step i's backward (W = 1)
+            nx = dev_batches[(i + 1) % POOL_BATCHES]
+            layer.lookup_prefetch(nx.ids, nx.offsets, nx.batch, nx.nnz, stream)
         layer.backward_update(db.dy, wl.lr, stream)
 
-    def barrier():
-        if n > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+    def max_ranks(x):
+        if n == 1:
+            return x
+        t = torch.tensor([x], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for i in range(args.warmup):
         step(i)
@@ -288,49 +355,39 @@ def main():
     # per-step statistics (unique counts) for the byte accounting, outside the timed region
     infos = []
     for i in range(POOL_BATCHES):
-        db = dev_batches[i]
-        layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
-        layer.backward_update(db.dy, wl.lr, stream)
+        step(i)
         infos.append(layer.step_info())  # launches counted over lookup + backward
     barrier()
-
-    # per-kernel CUDA events (libemb's profiler, recorded on the stream each kernel runs on) cost ~11 us
-    # of device time per step at C2 when on for every step, so they are on for every PROF_EVERY-th timed
-    # step only (the launch averages come from those sampled steps of the same timed loop)
-    noprof = bool(os.environ.get("EMB_BENCH_NOPROF"))  # experiment: no per-kernel events at all
-    PROF_EVERY = 8
-    layer.profile(True)   # allocates the profiler's event pool now, outside the timed region
+    layer.profile(True)  # allocates the profiler's event pool now, outside the timed region
     layer.profile(False)
     layer.profile_reset()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fwd_ev = []  # (start, end) of the forward on unprofiled steps, up to 64
-    ev_pool = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(64)]
     barrier()
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for i in range(args.steps):
-            db = dev_batches[i % POOL_BATCHES]
-            if not noprof:
-                layer.profile(i % PROF_EVERY == 0)
-            rec = (noprof or i % PROF_EVERY != 0) and len(fwd_ev) < len(ev_pool)
-            if rec:
-                fwd_ev.append(ev_pool[len(fwd_ev)])
-                fwd_ev[-1][0].record(stream)
-            layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
-            if rec:
-                fwd_ev[-1][1].record(stream)
-            prefetch_next(i)
-            layer.backward_update(db.dy, wl.lr, stream)
+            step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
-    t_ms = ev0.elapsed_time(ev1)
-    prof = {} if noprof else layer.profile_read()
-    layer.profile(False)
-    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev) if fwd_ev else float("nan")
-    if n > 1:
-        t = torch.tensor([t_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
+    t_ms = max_ranks(ev0.elapsed_time(ev1))
+    barrier()
+
+    # profiled loop (not part of the headline): per-kernel device times and the forward time
+    prof, fwd_ms = {}, float("nan")
+    if profile_steps > 0:
+        fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(profile_steps)]
+        layer.profile(True)
+        for i in range(profile_steps):
+            db = dev_batches[i % POOL_BATCHES]
+            fwd_ev[i][0].record(stream)
+            layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
+            fwd_ev[i][1].record(stream)
+            layer.backward_update(db.dy, wl.lr, stream)
+        torch.cuda.synchronize()
+        prof = layer.profile_read()
+        layer.profile(False)
+        fwd_ms = max_ranks(statistics.mean(a.elapsed_time(b) for a, b in fwd_ev))
         barrier()
 
     ms_step = t_ms / args.steps
@@ -340,7 +397,7 @@ def main():
     N_mean = statistics.mean(b.nnz for b in host_batches)
     SB = wl.num_slots * B
     U_l, U_o = mean("unique_local"), mean("unique_owner")
-    lookups_s = n * N_mean / (fwd_ms / 1e3)
+    lookups_s = n * N_mean / (fwd_ms / 1e3) if fwd_ms == fwd_ms else None
     peak, peak_src = _peaks()
     hbm = step_bytes(wl, N_mean, SB, U_l, U_o, n)
     launches_per_step = statistics.mean(inf["launches"] for inf in infos)
@@ -353,14 +410,28 @@ def main():
         t_launch = dom_ms / dom_cnt / 1e3
         ach = kb / t_launch / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": _traffic(dom) if n == 1 else None, "launch_us": round(t_launch * 1e6, 2),
-                "algorithmic_bytes_per_launch": int(kb), "peak_source": peak_src}
+                "frac": round(ach / peak, 4), "traffic": _traffic(dom, wl.opt) if n == 1 else None,
+                "launch_us": round(t_launch * 1e6, 2), "algorithmic_bytes_per_launch": int(kb),
+                "peak_source": peak_src,
+                "timing": f"CUDA events on the kernel's stream, {profile_steps} profiled steps after the timed loop"}
     kernels = {k: {"ms_total": round(v[0], 3), "launches": v[1], "us_per_launch": round(1e3 * v[0] / max(v[1], 1), 2)}
                for k, v in prof.items()}
+    nvl = None
+    if n > 1:
+        nb = nvlink_bytes(wl, U_l, n)
+        ex_us = sum(kernels[k]["us_per_launch"] for k in ("gather_push", "grad_push") if k in kernels)
+        nvl = {"bytes_per_step_per_direction": int(nb), "peak_gbs": 770.0,
+               "peak_source": "measured peer copy per direction, B200_PROFILING.md (900 nominal)",
+               "achieved_step_gbs": round(nb / (ms_step / 1e3) / 1e9, 1),
+               "frac_step": round(nb / (ms_step / 1e3) / 1e9 / 770.0, 4),
+               "exchange_kernels_us": round(ex_us, 2),
+               "frac_exchange_kernels": round(nb / (ex_us / 1e6) / 1e9 / 770.0, 4) if ex_us else None,
+               "note": "frac_exchange_kernels: NVLink bytes / (owner gather-push + requester-merge kernel "
+                       "times): the exchange phase's fraction of the link (those kernels also do HBM work)"}
 
     # e2e through the host-buffer C-ABI entry points (pinned host memory, copies inside the timed region)
     e2e = None
-    if args.e2e_steps > 0:
+    if e2e_steps > 0:
         hb = host_batches[0]
         ids_h = torch.from_numpy(hb.ids).pin_memory()
         off_h = torch.from_numpy(hb.offsets).pin_memory()
@@ -369,60 +440,39 @@ def main():
         for _ in range(2):
             layer.lookup_host(ids_h.numpy(), off_h.numpy(), B, hb.nnz, out_h.numpy(), stream)
             layer.backward_update_host(dy_h.numpy(), wl.lr, stream)
+        layer.host_sync()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.e2e_steps):
+        for _ in range(e2e_steps):
             layer.lookup_host(ids_h.numpy(), off_h.numpy(), B, hb.nnz, out_h.numpy(), stream)
             layer.backward_update_host(dy_h.numpy(), wl.lr, stream)
+        layer.host_sync()
         e1.record(stream)
         torch.cuda.synchronize()
-        te = e0.elapsed_time(e1)
-        if n > 1:
-            t = torch.tensor([te], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
-        e2e = {"value": n * B * args.e2e_steps / (te / 1e3), "unit": "samples/s",
+        te = max_ranks(e0.elapsed_time(e1))
+        e2e = {"value": n * B * e2e_steps / (te / 1e3), "unit": "samples/s",
                "h2d_bytes_per_step": int(hb.ids.nbytes + hb.offsets.nbytes + hb.dy.nbytes),
-               "d2h_bytes_per_step": int(out_h.numel() * 4), "ms_per_step": te / args.e2e_steps,
-               "path": "emb_lookup_host + emb_backward_update_host (pinned host buffers)"}
-
-    cpu = None
-    if rank == 0 and n == 1 and not args.no_cpu:  # the CPU baseline is an N = 1 figure
-        sps, lps, sample = oracle_time(wl, budget_s=args.cpu_budget)
-        thr, pool = cpu_threads()
-        cpu = {"value": sps, "unit": "samples/s", "cores": thr, "kind": "oracle",
-               "sample": sample + f"; host has {os.cpu_count()} cores, NumPy primitives single-threaded",
-               "lookups_per_s": lps}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": samples_s, "unit": "samples/s", "n_gpus": n, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 (fp64 accumulation)", "data": "synthetic",
-            "config": {"workload": describe(wl, n), "global_batch": n * B, "nnz_per_gpu": N_mean,
-                       "unique_local": U_l, "unique_owner": U_o,
-                       "l2": f"inputs larger than L2: {POOL_BATCHES} distinct staged batches cycled "
-                             f"({POOL_BATCHES} x {(hb_bytes(host_batches[0], wl)) / 1e6:.0f} MB) + "
-                             f"{layer.rows_local * 4 * (wl.dim + layer.accum_width * (wl.opt != 'sgd')) / 1e9:.1f} GB table "
-                             "state per GPU"},
-            "lookups_per_s": lookups_s,
-            "fwd_ms": fwd_ms,
-            "step_roofline": {"bound": "hbm", "algorithmic_bytes": int(hbm),
-                              "achieved": round(hbm / (ms_step / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
-                              "frac": round(hbm / (ms_step / 1e3) / 1e9 / peak, 4)},
-            "roofline": roof,
-            "kernels": kernels,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": int(round(launches_per_step * args.steps)),
-            "clocks": clk.summary(),
-        }
-        print(json.dumps(line), flush=True)
+               "d2h_bytes_per_step": int(out_h.numel() * 4), "ms_per_step": te / e2e_steps,
+               "path": "emb_lookup_host + emb_backward_update_host (pinned host buffers; H2D and D2H on the "
+                       "library's copy streams, double-buffered), emb_host_sync before the end event"}
+    config = {"workload": describe(wl, n), "global_batch": n * B, "nnz_per_gpu": N_mean,
+              "unique_local": U_l, "unique_owner": U_o,
+              "l2": f"inputs larger than L2: {POOL_BATCHES} distinct staged batches cycled "
+                    f"({POOL_BATCHES} x {(hb_bytes(host_batches[0], wl)) / 1e6:.0f} MB) + "
+                    f"{layer.rows_local * 4 * (wl.dim + layer.accum_width * (wl.opt != 'sgd')) / 1e9:.1f} GB table "
+                    "state per GPU"}
+    out = {"value": samples_s, "ms_per_step": ms_step, "config": config, "lookups_per_s": lookups_s,
+           "fwd_ms": fwd_ms,
+           "step_roofline": {"bound": "hbm", "algorithmic_bytes": int(hbm),
+                             "achieved": round(hbm / (ms_step / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                             "frac": round(hbm / (ms_step / 1e3) / 1e9 / peak, 4)},
+           "roofline": roof, "nvlink": nvl, "kernels": kernels, "e2e": e2e,
+           "gpu_launches": int(round(launches_per_step * args.steps)), "clocks": clk.summary()}
     layer.close()
-    if n > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    del dev_batches
+    torch.cuda.empty_cache()
+    return out
 
 
 def hb_bytes(bt, wl):

@@ -171,12 +171,20 @@ emb_status_t emb_lookup_group(emb_handle_t *hs, int32_t n, const int64_t *const 
 emb_status_t emb_backward_update_group(emb_handle_t *hs, int32_t n, const float *const *d_out, double lr,
                                        void *const *streams);
 
-/* End-to-end variants over HOST buffers (pinned recommended): copy the inputs host->device, run the
- * device call above on cuda_stream, copy the result device->host, and return after the stream work
- * completed. ids/offsets/out / d_out are host pointers with the layouts above. */
+/* End-to-end variants over HOST buffers (pinned memory, else the copies serialise): ASYNCHRONOUS --
+ * each call returns after enqueueing. emb_lookup_host copies ids/offsets host->device on the
+ * library's H2D copy stream into one of two staging sets, runs emb_lookup on cuda_stream after them,
+ * and copies out[] device->host on the library's D2H copy stream; emb_backward_update_host copies
+ * d_out host->device (H2D stream) and runs emb_backward_update on cuda_stream. With two staging sets
+ * the D2H of step k's output overlaps the H2D copies of step k's gradient and of step k+1's ids (the
+ * two PCIe directions). Host buffers must stay valid and unmodified, and out[] must not be read, until
+ * emb_host_sync(h) returns. Layouts as for the device calls. Argument / state errors are returned
+ * synchronously; device-detected errors as for the device calls. Not for group handles. */
 emb_status_t emb_lookup_host(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                              int64_t nnz, float *out, void *cuda_stream);
 emb_status_t emb_backward_update_host(emb_handle_t h, const float *d_out, double lr, void *cuda_stream);
+/* Wait until every host-buffer call of h completed (copies included); returns the sticky status. */
+emb_status_t emb_host_sync(emb_handle_t h);
 
 /* ---- host-synchronous helpers (tests, checkpoint, accounting; call between steps) ------------- */
 

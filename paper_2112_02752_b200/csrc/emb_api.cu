@@ -10,11 +10,13 @@
 //   backward : fused segment-reduce + optimizer apply over the sorted keys
 // Step at world > 1 (no host sync; e = the step's epoch, exchanges over peer memory, p2p.cu):
 //   lookup   : L0 sort -> k_route (keys into the owners' regions, counts + error bits, KEYS(e))
-//              L1 side: wait KEYS(e) -> owner merge of the W received runs
-//                 main: wait APPLIED(e-1) -> pull my remote distinct rows -> pool -> join
+//              L1 wait KEYS(e) -> side: owner merge of the W received runs
+//                                 main: gather the rows the others asked for, store them into their
+//                                       row regions (ROWS(e))
+//              L2 wait ROWS(e) -> pool -> join
 //   backward : B0 requester merge of duplicate-id gradients, rows stored into the owners' regions
 //                 (GRADS(e))
-//              B1 wait GRADS(e) -> owner merge over sources (source-rank order) + apply (APPLIED(e))
+//              B1 wait GRADS(e) -> owner merge over sources (source-rank order) + apply
 // Multi-process (one rank per process): a rank runs its phases back to back and the in-kernel flag
 // waits order it against its peers. Group mode (emb_create_group: all ranks in this process, any
 // devices, possibly one): emb_lookup_group / emb_backward_update_group run phase by phase over the
@@ -44,7 +46,7 @@ std::mutex g_err_mu;
 std::string g_create_error = "no error";
 
 const char *kKernelNames[KID_COUNT] = {"keys",      "sort_hist", "sort_pass", "pool",        "grad_apply",
-                                       "unique",    "route",     "pull",      "grad_push",   "signal",
+                                       "unique",    "route",     "gather_push", "grad_push",   "signal",
                                        "init",      "owner_merge", "p2p_wait"};
 
 uint32_t bits_for(uint64_t x) {  // smallest b with x < 2^b (x >= 0)
@@ -116,14 +118,13 @@ struct emb_ctx {
   int64_t cap = 0;                   // entries per source region: max over ranks of max_ids
   uint32_t *inv = nullptr;           // [max_ids] occurrence -> o*cap + sendpos
   uint32_t *outidx = nullptr;        // [max_ids] sorted position -> sendpos
-  uint32_t *send_local = nullptr;    // [W*cap] my distinct keys' local ids per owner region
   int64_t *scnt = nullptr;           // [P2P_MAXW] my per-owner counts (device)
   uint32_t *route_tot = nullptr, *route_counter = nullptr, *route_done = nullptr;
   uint64_t *route_status = nullptr;
   uint32_t route_tag = 0;
   uint32_t *recv_keys = nullptr;     // [2][W*cap] (peer-written)
-  float *uniq_rows = nullptr;        // [W*cap][D] pulled rows
-  float *grecv = nullptr;            // [2][W*cap][D] hi / lo parts (peer-written)
+  float *uniq_rows = nullptr;        // [W*cap][D] rows pushed by their owners (peer-written)
+  float *grecv = nullptr;            // [W*cap][2D] hi / lo parts, lane-interleaved (peer-written)
   uint32_t *ok0 = nullptr, *ov0 = nullptr, *ok1 = nullptr, *ov1 = nullptr;  // owner merge
   int64_t *n_merged = nullptr;       // device: keys received this step
   int64_t *xmat = nullptr;           // [2][2][P2P_MAXW] (peer-written)
@@ -154,12 +155,13 @@ struct emb_ctx {
   cudaStream_t last_stream = nullptr;
   int launches = 0;
 
-  // ---- host-buffer (e2e) staging, allocated on first use (two sets: double buffering)
+  // ---- host-buffer (e2e) path, allocated on first use: two staging sets (step k uses set k & 1), H2D
+  // copies on h2d_stream, D2H on d2h_stream (opposite PCIe directions overlap), events between them
   int64_t *st_ids[2] = {nullptr, nullptr}, *st_offsets[2] = {nullptr, nullptr};
   float *st_out[2] = {nullptr, nullptr}, *st_dout[2] = {nullptr, nullptr};
-  int st_set = 0;
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  int st_set = 0, host_set = 0;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr, host_stream = nullptr;
+  cudaEvent_t ev_h2d[2] = {}, ev_h2d2[2] = {}, ev_looked[2] = {}, ev_d2h[2] = {}, ev_free[2] = {};
 
   // ---- profiler
   bool prof_on = false;
@@ -250,7 +252,7 @@ void peer_buffers(emb_ctx *h, void *out[NB_PEER]) {
   out[1] = h->flags;
   out[2] = h->recv_keys;
   out[3] = h->grecv;
-  out[4] = h->w;
+  out[4] = h->uniq_rows;
 }
 void set_peer(emb_ctx *h, int r, void *const ptr[NB_PEER]) {
   P2PArgs &p = h->p2p;
@@ -258,7 +260,7 @@ void set_peer(emb_ctx *h, int r, void *const ptr[NB_PEER]) {
   p.peer_flags[r] = static_cast<uint64_t *>(ptr[1]);
   p.peer_recv_keys[r] = static_cast<uint32_t *>(ptr[2]);
   p.peer_grecv[r] = static_cast<float *>(ptr[3]);
-  p.peer_w[r] = static_cast<const float *>(ptr[4]);
+  p.peer_uniq_rows[r] = static_cast<float *>(ptr[4]);
 }
 void init_p2p_args(emb_ctx *h) {
   P2PArgs &p = h->p2p;
@@ -546,7 +548,6 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
   if (W > 1) {
     bad |= dalloc(h, &h->inv, N) != cudaSuccess;
     bad |= dalloc(h, &h->outidx, N) != cudaSuccess;
-    bad |= dalloc(h, &h->send_local, WC) != cudaSuccess;
     bad |= dalloc(h, &h->scnt, P2P_MAXW) != cudaSuccess;
     bad |= dalloc(h, &h->route_tot, P2P_MAXW) != cudaSuccess;
     bad |= dalloc(h, &h->route_counter, 1) != cudaSuccess;
@@ -585,6 +586,14 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
     h->segsort_ok = true;
     for (int s = 1; s < h->S; ++s)
       if (h->slot_table[s] < h->slot_table[s - 1]) h->segsort_ok = false;
+    int32_t ngroups = 0;
+    for (int s = 0; s < h->S; ++s) ngroups += (s == 0 || h->slot_table[s] != h->slot_table[s - 1]);
+    // the per-table sort keeps a group's key ranges in shared memory: K <= 16 CTAs per group, each
+    // scanning the whole group. Groups much larger than that (C4: 1.7M ids on one table; C5: 1M ids
+    // per table) take the general path instead -- key kernel + onesweep LSD radix sort over all keys
+    // (round 1 measured 7.6 ms of per-table sort at C5 against a few hundred us for the radix passes)
+    if (h->segsort_ok && (h->max_ids + ngroups - 1) / ngroups > (int64_t)SEG_BIG) h->segsort_ok = false;
+    if (const char *ef = getenv("EMB_FORCE_GENERAL")) if (atoi(ef)) h->segsort_ok = false;  // experiment knob
     if (h->segsort_ok) {
       std::vector<int32_t> gslot;
       std::vector<uint64_t> gbase;
@@ -658,11 +667,13 @@ void destroy_impl(emb_ctx *h) {
   for (void *p : h->allocs) cudaFree(p);
   if (h->err_host) cudaFreeHost(h->err_host);
   for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
-  for (cudaEvent_t e : {h->ev_fork, h->ev_join, h->ev_pf, h->ev_phase, h->ev_h2d[0], h->ev_h2d[1], h->ev_d2h[0],
-                        h->ev_d2h[1]})
+  for (cudaEvent_t e : {h->ev_fork, h->ev_join, h->ev_pf, h->ev_phase})
     if (e) cudaEventDestroy(e);
-  if (h->side) cudaStreamDestroy(h->side);
-  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  for (int k = 0; k < 2; ++k)
+    for (cudaEvent_t e : {h->ev_h2d[k], h->ev_h2d2[k], h->ev_looked[k], h->ev_d2h[k], h->ev_free[k]})
+      if (e) cudaEventDestroy(e);
+  for (cudaStream_t q : {h->side, h->h2d_stream, h->d2h_stream})
+    if (q) cudaStreamDestroy(q);
   delete h;
 }
 
@@ -864,7 +875,6 @@ emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
   ra.p2p = h->p2p;
   ra.outidx = h->outidx;
   ra.inv = h->inv;
-  ra.send_local = h->send_local;
   ra.scnt = h->scnt;
   ra.tot = h->route_tot;
   ra.status = h->route_status;
@@ -878,18 +888,24 @@ emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
   return EMB_OK;
 }
 
-// L1: owner merge (side stream, after KEYS) | pull (after APPLIED of the previous step) + pool
+// L1: wait KEYS -> owner merge (side stream) | gather + push the requested rows (raises ROWS)
 emb_status_t lookup_phase1(emb_ctx *h, cudaStream_t st) {
   const P2PArgs &px = h->p2p;
   const int W = h->world;
+  const uint32_t *rk = h->recv_keys + (size_t)(h->epoch & 1u) * W * h->cap;
+  const int64_t *cnt = h->xmat + xmat_idx(h->epoch, 0, 0);
+  LAUNCH(h, KID_WAIT, st, launch_wait(px, P2P_KEYS, h->epoch, h->err_dev, st));
   CUDA_TRY(h, cudaEventRecord(h->ev_fork, st));
   CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-  LAUNCH(h, KID_WAIT, h->side, launch_wait(px, P2P_KEYS, h->epoch, h->err_dev, h->side));
   LAUNCH(h, KID_MERGE, h->side,
-         launch_merge_tree(h->recv_keys + (size_t)(h->epoch & 1u) * W * h->cap, h->xmat + xmat_idx(h->epoch, 0, 0), W,
-                           h->cap, h->ok0, h->ov0, h->ok1, h->ov1, h->n_merged, h->side));
-  LAUNCH(h, KID_WAIT, st, launch_wait(px, P2P_APPLIED, h->epoch - 1, h->err_dev, st));
-  LAUNCH(h, KID_PULL, st, launch_pull(px, h->scnt, h->send_local, h->uniq_rows, h->D, std::max<int64_t>(h->nnz, 1), st));
+         launch_merge_tree(rk, cnt, W, h->cap, h->ok0, h->ov0, h->ok1, h->ov1, h->n_merged, h->side));
+  LAUNCH(h, KID_GATHER_PUSH, st, launch_gather_push(px, h->w, rk, cnt, h->D, h->rows_local, h->err_dev, st));
+  return EMB_OK;
+}
+
+// L2: wait ROWS -> pool; join the merge
+emb_status_t lookup_phase2(emb_ctx *h, cudaStream_t st) {
+  LAUNCH(h, KID_WAIT, st, launch_wait(h->p2p, P2P_ROWS, h->epoch, h->err_dev, st));
   if (h->batch > 0 && h->cur_out) {
     PoolArgs pa = pool_args(h, h->cur_ids, h->cur_offsets, h->batch, h->nnz, h->cur_out);
     LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
@@ -941,7 +957,6 @@ emb_status_t backward_phase0(emb_ctx *h, const float *d_out, double lr, cudaStre
   g.sink_mode = 2;
   g.useg = h->outidx;
   g.nout = h->cap;
-  g.lo_stride = (int64_t)h->world * h->cap * h->D;
   g.signal_kind = P2P_GRADS;
   if (h->batch > 0 && h->nnz > 0 && d_out)
     LAUNCH(h, KID_GRAD_PUSH, st, launch_grad(g, st));
@@ -950,7 +965,7 @@ emb_status_t backward_phase0(emb_ctx *h, const float *d_out, double lr, cudaStre
   return EMB_OK;
 }
 
-// B1: wait GRADS, owner merge over sources + apply (raises APPLIED)
+// B1: wait GRADS, owner merge over sources + apply
 emb_status_t backward_phase1(emb_ctx *h, double lr, cudaStream_t st) {
   const int W = h->world;
   GradArgs o = grad_args(h, nullptr, lr);
@@ -960,11 +975,11 @@ emb_status_t backward_phase1(emb_ctx *h, double lr, cudaStream_t st) {
   o.n_dev = h->n_merged;
   o.src_mode = 1;
   o.src = h->grecv;
-  o.src_lo = h->grecv + (size_t)W * h->cap * h->D;
+  o.src_lo = h->grecv;  // rows are 2D floats: hi / lo lane-interleaved (grad.cu store_hilo)
   o.nsrc = (int64_t)W * h->cap;
   o.blen = nullptr;
   o.sink_mode = 0;
-  o.signal_kind = P2P_APPLIED;
+  o.signal_kind = -1;
   o.skip_mask = EMB_DEVERR_TIMEOUT | EMB_DEVERR_INTERNAL;
   o.abort_bits = h->xmat + xmat_idx(h->epoch, 1, 0);
   LAUNCH(h, KID_WAIT, st, launch_wait(h->p2p, P2P_GRADS, h->epoch, h->err_dev, st));
@@ -1003,6 +1018,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   h->cur_out = *ae ? nullptr : out;
   emb_status_t r = lookup_phase0(h, st);
   if (r == EMB_OK) r = lookup_phase1(h, st);
+  if (r == EMB_OK) r = lookup_phase2(h, st);
   if (r != EMB_OK) return r;
   h->state = 1;
   if (*ae) return fail(h, EMB_ERR_INVALID, std::string(ae) + " (the rank took part with an empty batch; the step "
@@ -1125,9 +1141,11 @@ emb_status_t copy_unique(emb_ctx *h, const uint32_t *uend_dev, const uint32_t *u
   return EMB_OK;
 }
 
-// ---- host-buffer (e2e) path: double-buffered staging. The H2D copies of a call run on a copy stream
-// (so they can overlap the previous call's device work and D2H); the D2H of the result is enqueued on
-// the caller stream and the call returns after the stream work completed.
+// ---- host-buffer (e2e) path: double-buffered staging, asynchronous. A call returns after enqueueing:
+// the H2D copies of step k run on h2d_stream as soon as staging set k & 1 is free (its step k-2 backward
+// completed), the device work on the caller stream after them, the D2H of Y on d2h_stream after the
+// lookup -- so the D2H of Y_k overlaps the H2D of dY_k and of the ids of step k+1 (the two PCIe
+// directions). emb_host_sync waits for all of it.
 emb_status_t ensure_staging(emb_ctx *h) {
   if (h->st_ids[0]) return EMB_OK;
   const size_t SB = (size_t)h->S * h->max_batch;
@@ -1135,11 +1153,11 @@ emb_status_t ensure_staging(emb_ctx *h) {
     if (dalloc(h, &h->st_ids[k], h->max_ids) || dalloc(h, &h->st_offsets[k], SB + 1) ||
         dalloc(h, &h->st_out[k], SB * h->D) || dalloc(h, &h->st_dout[k], SB * h->D))
       return fail(h, EMB_ERR_NOMEM, "cannot allocate host-path staging");
-  CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-  for (int k = 0; k < 2; ++k) {
-    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_h2d[k], cudaEventDisableTiming));
-    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_d2h[k], cudaEventDisableTiming));
-  }
+  CUDA_TRY(h, cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
+  CUDA_TRY(h, cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k)
+    for (cudaEvent_t *e : {&h->ev_h2d[k], &h->ev_h2d2[k], &h->ev_looked[k], &h->ev_d2h[k], &h->ev_free[k]})
+      CUDA_TRY(h, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   return EMB_OK;
 }
 
@@ -1281,6 +1299,8 @@ emb_status_t emb_lookup_group(emb_handle_t *hs, int32_t n, const int64_t *const 
   emb_status_t s = group_phase(hs, n, streams, [](emb_ctx *h, int, cudaStream_t st) { return lookup_phase0(h, st); });
   if (s == EMB_OK)
     s = group_phase(hs, n, streams, [](emb_ctx *h, int, cudaStream_t st) { return lookup_phase1(h, st); });
+  if (s == EMB_OK)
+    s = group_phase(hs, n, streams, [](emb_ctx *h, int, cudaStream_t st) { return lookup_phase2(h, st); });
   if (s != EMB_OK) return s;
   for (int r = 0; r < n; ++r) hs[r]->state = 1;
   if (first_err != EMB_OK) return first_err;
@@ -1330,38 +1350,60 @@ emb_status_t emb_lookup_host(emb_handle_t h, const int64_t *ids, const int64_t *
   if (batch < 0 || batch > h->max_batch || nnz < 0 || nnz > h->max_ids)
     return fail(h, EMB_ERR_INVALID, "batch/nnz out of range");
   if ((batch > 0 && (!offsets || !out)) || (nnz > 0 && !ids)) return fail(h, EMB_ERR_INVALID, "NULL host buffer");
+  if (h->state != 0) return fail(h, EMB_ERR_STATE, "emb_lookup_host called twice without a backward");
   CUDA_TRY(h, cudaSetDevice(h->device));
   emb_status_t s = ensure_staging(h);
   if (s != EMB_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   const size_t SB = (size_t)h->S * batch;
   const int k = h->st_set;
-  if (nnz > 0) CUDA_TRY(h, cudaMemcpyAsync(h->st_ids[k], ids, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+  h->host_set = k;
+  h->st_set ^= 1;
+  h->host_stream = st;
+  // inputs into set k once its previous user (step k-2's backward) is done
+  CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_free[k], 0));
+  if (nnz > 0) CUDA_TRY(h, cudaMemcpyAsync(h->st_ids[k], ids, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, h->h2d_stream));
   if (batch > 0)
-    CUDA_TRY(h, cudaMemcpyAsync(h->st_offsets[k], offsets, sizeof(int64_t) * (SB + 1), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(h->st_offsets[k], offsets, sizeof(int64_t) * (SB + 1), cudaMemcpyHostToDevice,
+                                h->h2d_stream));
+  CUDA_TRY(h, cudaEventRecord(h->ev_h2d[k], h->h2d_stream));
+  CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_h2d[k], 0));
+  CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_d2h[k], 0));  // step k-2's Y left st_out[k]
   s = lookup_impl(h, h->st_ids[k], h->st_offsets[k], batch, nnz, h->st_out[k], st);
-  if (s != EMB_OK) return s;
-  if (batch > 0)
-    CUDA_TRY(h, cudaMemcpyAsync(out, h->st_out[k], sizeof(float) * SB * h->D, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(h, cudaStreamSynchronize(st));
-  return check_sticky(h);
+  if (s != EMB_OK && h->state != 1) return s;  // (at W > 1 a failed call still took part: copy what there is)
+  CUDA_TRY(h, cudaEventRecord(h->ev_looked[k], st));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->d2h_stream, h->ev_looked[k], 0));
+  if (batch > 0 && h->batch > 0)
+    CUDA_TRY(h, cudaMemcpyAsync(out, h->st_out[k], sizeof(float) * SB * h->D, cudaMemcpyDeviceToHost, h->d2h_stream));
+  CUDA_TRY(h, cudaEventRecord(h->ev_d2h[k], h->d2h_stream));
+  return s;
 }
 
 emb_status_t emb_backward_update_host(emb_handle_t h, const float *d_out, double lr, void *cuda_stream) {
   if (!h) return EMB_ERR_INVALID;
+  if (!h->st_ids[0] || h->state != 1)
+    return fail(h, EMB_ERR_STATE, "emb_backward_update_host without a preceding emb_lookup_host");
   CUDA_TRY(h, cudaSetDevice(h->device));
-  emb_status_t s = ensure_staging(h);
-  if (s != EMB_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   const size_t SB = (size_t)h->S * h->batch;
-  const int k = h->st_set;
-  if (h->state == 1 && h->batch > 0) {
+  const int k = h->host_set;
+  if (h->batch > 0) {
     if (!d_out) return fail(h, EMB_ERR_INVALID, "NULL d_out");
-    CUDA_TRY(h, cudaMemcpyAsync(h->st_dout[k], d_out, sizeof(float) * SB * h->D, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(h->st_dout[k], d_out, sizeof(float) * SB * h->D, cudaMemcpyHostToDevice, h->h2d_stream));
   }
-  s = emb_backward_update(h, h->st_dout[k], lr, st);
-  if (s != EMB_OK) return s;
-  CUDA_TRY(h, cudaStreamSynchronize(st));
+  CUDA_TRY(h, cudaEventRecord(h->ev_h2d2[k], h->h2d_stream));
+  CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_h2d2[k], 0));
+  emb_status_t s = emb_backward_update(h, h->st_dout[k], lr, st);
+  CUDA_TRY(h, cudaEventRecord(h->ev_free[k], st));
+  return s;
+}
+
+emb_status_t emb_host_sync(emb_handle_t h) {
+  if (!h) return EMB_ERR_INVALID;
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  if (h->h2d_stream) CUDA_TRY(h, cudaStreamSynchronize(h->h2d_stream));
+  if (h->host_stream) CUDA_TRY(h, cudaStreamSynchronize(h->host_stream));
+  if (h->d2h_stream) CUDA_TRY(h, cudaStreamSynchronize(h->d2h_stream));
   return check_sticky(h);
 }
 

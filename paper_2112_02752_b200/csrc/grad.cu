@@ -147,36 +147,50 @@ __device__ __forceinline__ void apply_rowwise(const GradArgs &a, const OptConst 
 // rank*cap + ui there (peer memory over NVLink, or this rank's own buffer when o == rank)
 __device__ __forceinline__ float *out_row3(const GradArgs &a, uint32_t key, uint32_t ui, int D) {
   const uint32_t o = owner_of_g(key, a.ks);
-  return a.p2p.peer_grecv[o] + (size_t)((int64_t)a.p2p.rank * a.p2p.cap + ui) * D;
+  return a.p2p.peer_grecv[o] + (size_t)((int64_t)a.p2p.rank * a.p2p.cap + ui) * (2 * D);  // (hi/lo rows)
 }
 
 // a merged per-key partial crosses the exchange as a double-float pair: hi = fp32(G), lo = fp32(G - hi)
 // (hi + lo carries ~48 bits, so partials of different ranks that cancel at the owner keep the fp64
-// result; an fp32 partial alone failed the tolerance on hot keys, reading R11'' in DESIGN.md). The lo
-// row sits lo_stride floats after the hi row.
+// result; an fp32 partial alone failed the tolerance on hot keys, reading R11'' in DESIGN.md). Rows of
+// the owner's region are 2D floats, lane-interleaved: lane l's 2*CPL floats (its CPL hi values, then
+// its CPL lo values) sit at 2*l*CPL, so each lane stores (and the owner's lane loads) one contiguous
+// 16*CPL/2-byte piece -- 128-bit peer stores.
 template <int CPL>
-__device__ __forceinline__ void store_hilo(const GradArgs &a, float *dst, const double (&g)[CPL]) {
-  VecF<CPL> hi, lo;
+__device__ __forceinline__ void store_hilo(float *dst, const double (&g)[CPL]) {
+  float o[2 * CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
-    hi.v[c] = (float)g[c];
-    lo.v[c] = (float)__dsub_rn(g[c], (double)hi.v[c]);
+    o[c] = (float)g[c];
+    o[CPL + c] = (float)__dsub_rn(g[c], (double)o[c]);
   }
-  stg_frag<CPL>(dst, hi);
-  stg_frag<CPL>(dst + a.lo_stride, lo);
+#pragma unroll
+  for (int c = 0; c < 2 * CPL; c += 4)
+    asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + c), "f"(o[c]), "f"(o[c + 1]), "f"(o[c + 2]),
+                 "f"(o[c + 3])
+                 : "memory");
 }
 
-// the last warp of the grid to finish raises the exchange flag (after every warp fenced its stores)
-__device__ __forceinline__ void grad_signal_last_warp(const GradArgs &a, int64_t nwarps) {
-  __threadfence_system();
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) {
+// the last CTA of the grid to finish raises the exchange flag: one system-scope fence per CTA, by the
+// thread that counts the CTA in, after the barrier (the CTA's stores happen before it). A fence in
+// every thread, then in every warp, made membar / ERRBAR the top stall of the requester pass (ncu,
+// profiles/r02_ncu_w2_group*.txt).
+__device__ __forceinline__ void grad_signal_last_cta(const GradArgs &a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
     const uint32_t t = atomicAdd(a.p2p.done + a.signal_kind, 1u);
-    if (t == (uint32_t)nwarps - 1) {
+    if (t == gridDim.x - 1) {
       a.p2p.done[a.signal_kind] = 0;
       p2p_raise(a.p2p, a.signal_kind);
     }
   }
+}
+
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t *p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
 // warp-parallel gallop: first (dir = -1) or last (dir = +1) position of the segment of key k that
@@ -227,19 +241,19 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
   }
   const int64_t first = seg_bound_warp(a.skey, n, pos, key, -1);
   const int64_t lastp = seg_bound_warp(a.skey, n, pos, key, +1);
-  __threadfence();
+  // the warp's partial stores happen before lane 0's release (syncwarp); the last arriver's acquire
+  // happens before its lanes' partial loads (syncwarp after the broadcast). acq_rel atomics instead of
+  // two gpu-scope fences per piece (ERRBAR stalls, profiles/r02_ncu_w2_group_b.txt).
   __syncwarp();
   int last = 0;
   const int64_t w0 = first / R, w1 = lastp / R;
   if (lane == 0) {
-    const uint32_t t = atomicAdd(&a.tickets[first], 1u);
+    const uint32_t t = atom_add_acq_rel(&a.tickets[first], 1u);
     last = (t == (uint32_t)(w1 - w0));
-    if (last) {
-      a.tickets[first] = 0;  // ready for the next step
-      __threadfence();
-    }
+    if (last) a.tickets[first] = 0;  // ready for the next step (kernel boundary orders it)
   }
   last = __shfl_sync(0xffffffffu, last, 0);
+  __syncwarp();
   if (!last) return;
   if (MODE != 4 && !active) return;  // (row-wise Adagrad reduces over the whole warp)
   double tot[CPL];
@@ -255,8 +269,7 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
     }
   }
   if constexpr (MODE == 3) {
-    store_hilo<CPL>(a, out_row3(a, key, a.useg[pos], D) + col, tot);
-    __threadfence_system();
+    store_hilo<CPL>(out_row3(a, key, a.useg[pos], D) + 2 * col, tot);
   } else if constexpr (MODE == 4) {
     const uint32_t lrow = key & a.lmask;
     const size_t off = (size_t)lrow * D + col;
@@ -308,10 +321,7 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
   const int64_t R = (n + nwarps - 1) / nwarps;
   const int64_t p_lo = gw * R;
   const int64_t p_hi = (p_lo + R < n) ? p_lo + R : n;
-  if (p_lo >= p_hi) {
-    if (a.signal_kind >= 0) grad_signal_last_warp(a, nwarps);
-    return;
-  }
+  if (p_lo < p_hi) {  // (no early return: the end-of-grid signal below is CTA-collective)
   const float *src_base = a.src_mode == 0 ? a.dy : a.src;
   const OptConst oc = opt_const(a);
 
@@ -335,8 +345,15 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
     if (a.src_mode != 0) return pay;
     return pay < (uint64_t)a.nsrc_occ ? a.drow[pay] : 0xFFFFFFFEu;
   };
+  // MODE 3: the key's rank in its owner's list, loaded with the source row (NS+1 tiles ahead: a load
+  // consumed in the same tile stalled the warp for a full memory latency per tile)
+  auto load_uo = [&](int64_t j) -> uint32_t {
+    if (MODE != 3) return 0;
+    const int64_t p = p_lo + j * T + lane;
+    return (j < ntile && lane < T && p < p_hi) ? a.useg[p] : 0u;
+  };
   // flags + async copies of tile j into stage s (keys k, source rows srow; knext_tile = first key of tile j+1)
-  auto issue = [&](int64_t j, int s, TileMeta &m, uint32_t k, uint32_t srow, uint32_t knext_tile) {
+  auto issue = [&](int64_t j, int s, TileMeta &m, uint32_t k, uint32_t srow, uint32_t uo_in, uint32_t knext_tile) {
     const int64_t t0 = p_lo + j * T;
     const int cnt = (int)((p_hi - t0) < T ? (p_hi - t0) : T);
     int32_t len = 1;
@@ -346,7 +363,7 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
       else if (MEAN) len = a.blen[srow];
       if (SINK_OPT && (int64_t)(k & a.lmask) >= a.nrows) bad = true;
       if (!SINK_OPT) {
-        uo = a.useg[t0 + lane];
+        uo = uo_in;
         if ((int64_t)uo >= a.nout) bad = true;
       }
     }
@@ -369,22 +386,27 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
     m.len = len;
     m.uo = uo;
     // async copies: chunk q = it*32 + lane of the tile's rows, row i = q / C16, 16-B chunk c = q % C16
+    // (a LO contribution row -- hi/lo interleaved -- is 2D floats)
     const uint32_t sb = wbase + (uint32_t)(s * stage_floats * 4);
-    const unsigned long long wrow = (unsigned long long)(k & a.lmask) * D;
-    for (int q0 = 0; q0 < T * C16; q0 += 32) {
+    constexpr int RW = LO ? 2 : 1;  // contribution row width in units of D
+    for (int q0 = 0; q0 < T * C16 * RW; q0 += 32) {
       const int q = q0 + lane;
-      const int i = q / C16, c = q - i * C16;
-      const int il = i < T ? i : 0;
-      const uint32_t ri = __shfl_sync(0xffffffffu, srow, il);
-      const unsigned long long wri = __shfl_sync(0xffffffffu, wrow, il);
-      const uint32_t off = (uint32_t)((i * D + c * 4) * 4);
-      if (i < T && ((m.vmask >> i) & 1u)) {
-        cp_async16(sb + off, src_base + (size_t)ri * D + c * 4);
-        if (LO) cp_async16(sb + (uint32_t)(T * D * 4) + off, a.src_lo + (size_t)ri * D + c * 4);
-      }
-      if (SINK_OPT && i < T && ((amask >> i) & 1u)) {
-        cp_async16(sb + (uint32_t)(OFF_W * D * 4) + off, a.w + wri + c * 4);
-        if (MODE == 1) cp_async16(sb + (uint32_t)(OFF_A * D * 4) + off, a.a + wri + c * 4);
+      const int i = q / (C16 * RW), c = q - i * (C16 * RW);
+      const uint32_t ri = __shfl_sync(0xffffffffu, srow, i < T ? i : 0);
+      if (i < T && ((m.vmask >> i) & 1u))
+        cp_async16(sb + (uint32_t)((i * RW * D + c * 4) * 4), src_base + (size_t)ri * (RW * D) + c * 4);
+    }
+    if (SINK_OPT) {
+      const unsigned long long wrow = (unsigned long long)(k & a.lmask) * D;
+      for (int q0 = 0; q0 < T * C16; q0 += 32) {
+        const int q = q0 + lane;
+        const int i = q / C16, c = q - i * C16;
+        const unsigned long long wri = __shfl_sync(0xffffffffu, wrow, i < T ? i : 0);
+        const uint32_t off = (uint32_t)((i * D + c * 4) * 4);
+        if (i < T && ((amask >> i) & 1u)) {
+          cp_async16(sb + (uint32_t)(OFF_W * D * 4) + off, a.w + wri + c * 4);
+          if (MODE == 1) cp_async16(sb + (uint32_t)(OFF_A * D * 4) + off, a.a + wri + c * 4);
+        }
       }
     }
     if (MODE == 4 && lane < T && ((amask >> lane) & 1u))  // the row's accumulator (4 bytes)
@@ -393,17 +415,20 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
 
   TileMeta meta[NS];
   // prologue: keys of tiles 0..NS+1, rows of tiles 0..NS, copies of tiles 0..NS-1 (one group each)
-  uint32_t kk[NS + 2], pp[NS + 2], rr[NS + 1];
+  uint32_t kk[NS + 2], pp[NS + 2], rr[NS + 1], uu[NS + 1];
 #pragma unroll
   for (int j = 0; j < NS + 2; ++j) load_kp(j, kk[j], pp[j]);
 #pragma unroll
-  for (int j = 0; j < NS + 1; ++j) rr[j] = load_row(kk[j], pp[j]);
+  for (int j = 0; j < NS + 1; ++j) {
+    rr[j] = load_row(kk[j], pp[j]);
+    uu[j] = load_uo(j);
+  }
 #pragma unroll
   for (int j = 0; j < NS; ++j) {
-    if (j < ntile) issue(j, j, meta[j], kk[j], rr[j], __shfl_sync(0xffffffffu, kk[j + 1], 0));
+    if (j < ntile) issue(j, j, meta[j], kk[j], rr[j], uu[j], __shfl_sync(0xffffffffu, kk[j + 1], 0));
     cp_async_commit();
   }
-  uint32_t k2 = kk[NS], r2 = rr[NS], k3 = kk[NS + 1], p3 = pp[NS + 1];
+  uint32_t k2 = kk[NS], r2 = rr[NS], u2 = uu[NS], k3 = kk[NS + 1], p3 = pp[NS + 1];
 
   DAcc<CPL> acc;
 #pragma unroll
@@ -438,21 +463,24 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
         for (int c = 0; c < CPL; ++c) acc.v[c] = hd ? 0.0 : acc.v[c];
         begins = begins || hd;
         VecF<CPL> v;
-        if (active) lds_frag<CPL>(v, sbase + 4u * (uint32_t)(i * D));
-        else v.zero();
-        if constexpr (LO) {  // a received per-key partial = hi + lo (double-float, R11'')
-          VecF<CPL> vl;
-          if (active) lds_frag<CPL>(vl, sbase + 4u * (uint32_t)((T + i) * D));
-          else vl.zero();
+        if constexpr (LO) {  // a received per-key partial = hi + lo (double-float, R11''), lane-interleaved
+          VecF<2 * CPL> hl;
+          if (active) lds_frag<2 * CPL>(hl, sbase + 4u * (uint32_t)(2 * i * D + col));  // (sbase has +4*col)
+          else hl.zero();
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) acc.v[c] = __dadd_rn(__dadd_rn(acc.v[c], (double)v.v[c]), (double)vl.v[c]);
+          for (int c = 0; c < CPL; ++c)
+            acc.v[c] = __dadd_rn(__dadd_rn(acc.v[c], (double)hl.v[c]), (double)hl.v[CPL + c]);
         } else if constexpr (MEAN) {
+          if (active) lds_frag<CPL>(v, sbase + 4u * (uint32_t)(i * D));
+          else v.zero();
           const int32_t li = __shfl_sync(0xffffffffu, m.len, i);
           const double dl = (double)li;
 #pragma unroll
           for (int c = 0; c < CPL; ++c)
             acc.v[c] = __dadd_rn(acc.v[c], li > 1 ? __ddiv_rn((double)v.v[c], dl) : (double)v.v[c]);
         } else {
+          if (active) lds_frag<CPL>(v, sbase + 4u * (uint32_t)(i * D));
+          else v.zero();
 #pragma unroll
           for (int c = 0; c < CPL; ++c) acc.v[c] = __dadd_rn(acc.v[c], (double)v.v[c]);
         }
@@ -461,7 +489,7 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
           if (begins) {  // complete inside the range
             if constexpr (!SINK_OPT) {
               const uint32_t ui = __shfl_sync(0xffffffffu, m.uo, i);
-              if (active) store_hilo<CPL>(a, out_row3(a, ki, ui, D) + col, acc.v);
+              if (active) store_hilo<CPL>(out_row3(a, ki, ui, D) + 2 * col, acc.v);
             } else if constexpr (MODE == 4) {
               VecF<CPL> wv;
               if (active) lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((OFF_W + i) * D));
@@ -498,22 +526,24 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
         open = false;
       }
       __syncwarp();  // every lane is done reading the stage before it is refilled
-      if (ti + NS < ntile) issue(ti + NS, s, m, k2, r2, __shfl_sync(0xffffffffu, k3, 0));
+      if (ti + NS < ntile) issue(ti + NS, s, m, k2, r2, u2, __shfl_sync(0xffffffffu, k3, 0));
       cp_async_commit();  // (possibly empty) group keeps the wait_group accounting uniform
       // advance the metadata pipeline: rows of tile ti+NS+1, keys of tile ti+NS+2
       const uint32_t r3 = load_row(k3, p3);
+      const uint32_t u3 = load_uo(ti + NS + 1);
       uint32_t k4, p4;
       load_kp(ti + NS + 2, k4, p4);
       k2 = k3;
       r2 = r3;
+      u2 = u3;
       k3 = k4;
       p3 = p4;
     }
   }
   cp_async_wait<0>();
   if (open && !broken) span_piece<CPL, MODE>(a, acc, begins ? 2 * gw + 1 : 2 * gw, open_pos, open_key, R, n);  // continues past the range
-  if (MODE == 3) __threadfence_system();  // peer stores of this thread precede the GRADS flag
-  if (a.signal_kind >= 0) grad_signal_last_warp(a, nwarps);
+  }  // p_lo < p_hi
+  if (a.signal_kind >= 0) grad_signal_last_cta(a);
 }
 
 static int g_sms = 0;

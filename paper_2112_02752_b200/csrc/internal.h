@@ -37,7 +37,7 @@ enum KernelId {
   KID_GRAD_APPLY,
   KID_UNIQUE,
   KID_ROUTE,
-  KID_PULL,
+  KID_GATHER_PUSH,
   KID_GRAD_PUSH,
   KID_SIGNAL,
   KID_INIT,
@@ -52,7 +52,7 @@ enum KernelId {
 // sources' runs end. Flags are per-(kind, source) epoch words raised in every peer; a wait requires
 // EXACTLY the expected epoch (a rank that fell behind times out instead of reading stale buffers).
 constexpr int P2P_MAXW = 16;  // == EMB_MAX_WORLD
-enum { P2P_KEYS = 0, P2P_GRADS = 1, P2P_APPLIED = 2, P2P_NKIND = 3 };
+enum { P2P_KEYS = 0, P2P_ROWS = 1, P2P_GRADS = 2, P2P_NKIND = 3 };
 // xmat layout (int64): [parity][0][s] = keys received from source s, [parity][1][s] = input-error
 // bits of source s in this step (parity = epoch & 1: double-buffered, a fast peer may already write
 // step e+1 while this rank still reads step e)
@@ -69,25 +69,28 @@ struct P2PArgs {
   uint64_t *peer_flags[P2P_MAXW];
   int64_t *peer_xmat[P2P_MAXW];
   uint32_t *peer_recv_keys[P2P_MAXW];   // [2][W * cap] owner-local ids, region s = source s
-  float *peer_grecv[P2P_MAXW];          // [2][W * cap][D] merged per-key gradients (hi, then lo parts),
-                                        // region s = source s
-  const float *peer_w[P2P_MAXW];        // table shards (the requester pulls its remote rows)
+  float *peer_grecv[P2P_MAXW];          // [W * cap][2D] merged per-key gradients as double-float
+                                        // (hi / lo lane-interleaved), region s = source s
+  float *peer_uniq_rows[P2P_MAXW];      // [W * cap][D] rows received by the requester, region o = owner o
 };
 // wait (one thread, bounded) until every source raised `kind` with exactly `epoch`
 cudaError_t launch_wait(const P2PArgs &a, int kind, uint64_t epoch, uint32_t *err, cudaStream_t st);
 // raise `kind` in every peer (a producer with nothing to do); err_bits != 0 are first OR-ed into every
 // owner's error slot of this step (xmat[parity][1][rank]): the owners then skip the update
 cudaError_t launch_signal(const P2PArgs &a, int kind, uint32_t err_bits, cudaStream_t st);
-// requester: uniq_rows[o*cap + i] = peer_w[o][send_local[o*cap + i]] for every remote owner o and
-// i < scnt[o] (peer loads over NVLink)
-cudaError_t launch_pull(const P2PArgs &a, const int64_t *scnt, const uint32_t *send_local, float *uniq_rows,
-                        int dim, int64_t max_rows, cudaStream_t st);
+// owner (A6 + X2 fused): for every source s != rank and i < xmat[s] (keys received from s this step),
+// the table row of local id recv_keys[s*cap + i] is stored straight into requester s's row region for
+// this owner, peer_uniq_rows[s][rank*cap + i] (peer stores over NVLink); the last block raises ROWS.
+// (Peer LOADS through CUDA-IPC mappings measured 19 GB/s against 600 GB/s for peer stores,
+// profiles/r02_ipc_gather_bench.log, so rows are pushed by the owner, not pulled by the requester.)
+cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t *recv_keys, const int64_t *counts,
+                               int dim, int64_t rows_local, uint32_t *err, cudaStream_t st);
 
 // A3+A4 fused (route.cu): over the sorted fused keys, per distinct key (segment head) its owner o and
 // its rank `sendpos` among this rank's distinct keys owned by o (ascending g); the head's local id is
 // stored straight into owner o's receive region; per sorted position outidx = sendpos; per
-// occurrence inv = o*cap + sendpos. The last block publishes the per-owner counts and this rank's
-// input-error bits into every owner's xmat and raises KEYS.
+// occurrence inv = o*cap + sendpos (the row owner o pushes back). The last block publishes the
+// per-owner counts and this rank's input-error bits into every owner's xmat and raises KEYS.
 struct RouteArgs {
   const uint32_t *skey, *spay;
   int64_t n;
@@ -95,7 +98,6 @@ struct RouteArgs {
   P2PArgs p2p;
   uint32_t *outidx;       // [n]
   uint32_t *inv;          // [max_ids] by occurrence
-  uint32_t *send_local;   // [W * cap]
   int64_t *scnt;          // [P2P_MAXW] out
   uint32_t *tot;          // [P2P_MAXW] zero on entry, left zero
   uint64_t *status;       // [tiles][P2P_MAXW] look-back words (epoch-tagged: no per-launch memset)
@@ -143,7 +145,7 @@ cudaError_t radix_sort_pairs(const SortWorkspace &ws, const uint32_t *kin, const
                              ProfHook prof, void *prof_ctx);
 
 // forward pool: Y[b][s][:] = sum (mean) over the bag's rows. A row g owned by this rank is read from
-// the table shard at local(g); at W > 1 a row owned by another rank from the pulled rows at inv[j].
+// the table shard at local(g); at W > 1 a row owned by another rank from the rows its owner pushed.
 struct PoolArgs {
   // direct mode (ids != nullptr, monotone slot -> table map): the pool validates the CSR and ids
   // itself, computes g = base[t] + id, and writes the per-occurrence dY row index (drow) and bag
@@ -162,7 +164,7 @@ struct PoolArgs {
   KeySpace ks;
   const float *rows_src;   // the table shard
   int64_t nrows_src;       // rows_local (bounds guard)
-  const float *rows_remote;  // W > 1: pulled rows [W*cap][D]
+  const float *rows_remote;  // W > 1: rows pushed by their owners [W*cap][D]
   int64_t nrows_remote;      // W * cap (bounds guard)
   const uint32_t *row_idx; // W > 1: inv (occurrence -> o*cap + sendpos) for rows owned elsewhere
   float *out;
@@ -190,8 +192,8 @@ struct GradArgs {
   const int32_t *blen;     // [B*S] bag length by dY row (mean) or nullptr
   int32_t batch, num_slots;
   const float *src;        // mode 1
-  const float *src_lo;     // mode 1, W > 1 owner side: low parts of the received double-float partials
-  int64_t lo_stride;       // sink 2: floats from a hi row to its lo row in the owner's region
+  const float *src_lo;     // non-null (W > 1 owner side): src rows are 2D-float double-float partials
+                           // (hi / lo lane-interleaved, grad.cu store_hilo)
   // sink: 0 = optimizer apply on table rows (row = key & lmask); 2 = the merged fp32 row stored
   // straight into the owner's gradient region through peer memory (requester side at W > 1)
   int32_t sink_mode;
@@ -243,6 +245,7 @@ cudaError_t launch_rows_scatter(float *dst, const int64_t *rows, int64_t n, int3
 
 // per-table stable sort (world == 1 fast path), see segsort.cu
 constexpr int64_t SEG_CAP = 16384;
+constexpr int64_t SEG_BIG = 65536;  // average ids per table group above which the general sort path runs
 struct SegSortArgs {
   const int64_t *ids;       // [nnz] table-local ids in CSR order (validated here: out of range = invalid)
   const int64_t *offsets;   // [S*B+1]

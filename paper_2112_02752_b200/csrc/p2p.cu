@@ -1,19 +1,20 @@
 // p2p.cu — the world > 1 exchange over NVLink peer memory (the synchronous analogue of
-// the paper's push-pull PS executor: a worker pulls the rows it needs and
+// the paper's push-pull PS executor: a worker receives the rows it needs and
 // pushes its gradients to the rows' owner).
 //
-// Every rank maps its peers' exchange buffers and table shard once at create (CUDA IPC handles
-// all-gathered over NCCL, or plain pointers when all ranks live in one process). One step, no host
-// synchronisation (e = the step's epoch):
+// Every rank maps its peers' exchange buffers once at create (CUDA IPC handles all-gathered over NCCL,
+// or plain pointers when all ranks live in one process). Every transfer is a peer STORE: peer loads
+// through CUDA-IPC mappings measured 19 GB/s against 600 GB/s for stores (profiles/r02_ipc_gather_bench.log).
+// One step, no host synchronisation (e = the step's epoch):
 //   A3+A4 k_route (route.cu): my distinct keys -> each owner's receive region for me; per-owner
 //                counts + my input-error bits -> every owner's xmat; raises KEYS(e).
 //   A5    owner: wait KEYS(e), stable merge of the W received runs (side stream).
-//   A6    k_pull: wait APPLIED(e-1) (every owner finished the previous update), then read my remote
-//                distinct rows straight from the owners' shards over NVLink.
+//   A6    k_gather_push: owner gathers the rows every other rank asked for and stores them into that
+//                rank's row region for me; raises ROWS(e). The requester waits ROWS(e), then pools
+//                (rows it owns straight from its shard).
 //   B2    k_grad MODE 3 (grad.cu): my merged per-key gradients -> each owner's gradient region for
 //                me; raises GRADS(e).
-//   B3+B4 owner: wait GRADS(e), merge the W sources per row in source-rank order + apply; raises
-//                APPLIED(e).
+//   B3+B4 owner: wait GRADS(e), merge the W sources per row in source-rank order + apply.
 // Ordering: writers fence at system scope; the last block (or warp) of the producing kernel raises the
 // per-(kind, source) epoch flag in every peer (p2p_dev.cuh); a one-thread k_wait spins (bounded) on the
 // flags before the consuming kernel runs on the same stream.
@@ -46,43 +47,44 @@ cudaError_t launch_wait(const P2PArgs &a, int kind, uint64_t epoch, uint32_t *er
   return cudaGetLastError();
 }
 
-// A6 pull: uniq_rows[o*cap + i][:] = peer_w[o][send_local[o*cap + i]][:] for every remote owner o,
-// i < scnt[o]. A row is D/4 float4 chunks; the flattened (row, chunk) index space of all remote
-// owners is walked grid-stride with PULL_UNROLL independent peer loads in flight per thread before
-// the stores (NVLink round trips are long; the loads of a thread are independent).
+// A6 + X2: the owner gathers its rows for every other source's received keys and stores them straight
+// into that requester's row region for this owner. A row is D/4 float4 chunks; the flattened (row,
+// chunk) space of all sources != rank is walked grid-stride with GP_UNROLL independent table loads in
+// flight per thread before the peer stores. The last block raises ROWS.
 namespace {
-constexpr int PULL_THREADS = 256;
-constexpr int PULL_UNROLL = 4;
+constexpr int GP_THREADS = 256;
+constexpr int GP_UNROLL = 4;
 }  // namespace
 
-__global__ void __launch_bounds__(PULL_THREADS) k_pull(P2PArgs a, const int64_t *__restrict__ scnt,
-                                                       const uint32_t *__restrict__ send_local,
-                                                       float4 *__restrict__ uniq_rows, int d4) {
+__global__ void __launch_bounds__(GP_THREADS) k_gather_push(P2PArgs a, const float4 *__restrict__ w,
+                                                            const uint32_t *__restrict__ recv_keys,
+                                                            const int64_t *__restrict__ counts, int d4,
+                                                            int64_t rows_local, uint32_t *err) {
   __shared__ int64_t pre[P2P_MAXW + 1];
-  __shared__ int32_t own[P2P_MAXW];
+  __shared__ int32_t src[P2P_MAXW];
   const int W = a.world;
-  if (threadIdx.x == 0) {  // compact prefix over the remote owners
+  if (threadIdx.x == 0) {  // compact prefix over the other sources
     int64_t s = 0;
     int q = 0;
     for (int o = 0; o < W; ++o) {
       if (o == a.rank) continue;
       pre[q] = s;
-      own[q] = o;
-      s += scnt[o];
+      src[q] = o;
+      s += counts[o];
       ++q;
     }
     pre[q] = s;
-    for (int r = q + 1; r <= P2P_MAXW; ++r) pre[r] = s;
   }
   __syncthreads();
   const int nq = W - 1;
   const int64_t total = pre[nq] * d4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < total; t0 += stride * PULL_UNROLL) {
-    float4 v[PULL_UNROLL];
-    float4 *dst[PULL_UNROLL];
+  bool bad = false;
+  for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < total; t0 += stride * GP_UNROLL) {
+    float4 v[GP_UNROLL];
+    float4 *dst[GP_UNROLL];
 #pragma unroll
-    for (int u = 0; u < PULL_UNROLL; ++u) {
+    for (int u = 0; u < GP_UNROLL; ++u) {
       const int64_t t = t0 + u * stride;
       dst[u] = nullptr;
       if (t < total) {
@@ -90,28 +92,35 @@ __global__ void __launch_bounds__(PULL_THREADS) k_pull(P2PArgs a, const int64_t 
         const int c = (int)(t - r * d4);
         int q = 0;
         while (q + 1 < nq && r >= pre[q + 1]) ++q;
-        const int o = own[q];
-        const int64_t slot = (int64_t)o * a.cap + (r - pre[q]);
-        const uint32_t lr = send_local[slot];
-        v[u] = ld_nc_f4(reinterpret_cast<const float4 *>(a.peer_w[o]) + (size_t)lr * d4 + c);
-        dst[u] = uniq_rows + (size_t)slot * d4 + c;
+        const int s = src[q];
+        const int64_t i = r - pre[q];
+        const uint32_t lr = recv_keys[(int64_t)s * a.cap + i];
+        if ((int64_t)lr >= rows_local) {
+          bad = true;
+          continue;
+        }
+        v[u] = ld_nc_f4(w + (size_t)lr * d4 + c);
+        dst[u] = reinterpret_cast<float4 *>(a.peer_uniq_rows[s]) + (size_t)((int64_t)a.rank * a.cap + i) * d4 + c;
       }
     }
 #pragma unroll
-    for (int u = 0; u < PULL_UNROLL; ++u)
+    for (int u = 0; u < GP_UNROLL; ++u)
       if (dst[u]) *dst[u] = v[u];
   }
+  if (bad) atomicOr(err, EMB_DEVERR_INTERNAL);
+  p2p_signal_last_block(a, P2P_ROWS);
 }
 
-cudaError_t launch_pull(const P2PArgs &a, const int64_t *scnt, const uint32_t *send_local, float *uniq_rows,
-                        int dim, int64_t max_rows, cudaStream_t st) {
-  if (a.world <= 1) return cudaSuccess;
+cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t *recv_keys, const int64_t *counts,
+                               int dim, int64_t rows_local, uint32_t *err, cudaStream_t st) {
   const int d4 = dim / 4;
-  int64_t blocks = (max_rows * d4 + PULL_THREADS * PULL_UNROLL - 1) / (PULL_THREADS * PULL_UNROLL);
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  int64_t blocks = ((int64_t)a.world * a.cap * d4 + GP_THREADS * GP_UNROLL - 1) / (GP_THREADS * GP_UNROLL);
+  // 4 blocks per SM keep ~64 KB of row loads in flight per SM (enough for the NVLink stores:
+  // profiles/r02_peer_gather_bench.log) and leave warp slots for the concurrent owner merge
+  if (blocks > 148 * 4) blocks = 148 * 4;
   if (blocks < 1) blocks = 1;
-  k_pull<<<(unsigned)blocks, PULL_THREADS, 0, st>>>(a, scnt, send_local, reinterpret_cast<float4 *>(uniq_rows),
-                                                    d4);
+  k_gather_push<<<(unsigned)blocks, GP_THREADS, 0, st>>>(a, reinterpret_cast<const float4 *>(w), recv_keys, counts,
+                                                         d4, rows_local, err);
   return cudaGetLastError();
 }
 

@@ -41,11 +41,13 @@ __device__ __forceinline__ void p2p_raise(const P2PArgs &a, int kind) {
   for (int p = 0; p < a.world; ++p) st_sys_u64(a.peer_flags[p] + kind * P2P_MAXW + a.rank, a.epoch);
 }
 
-// block epilogue: after the block's peer stores, the last block to finish raises flag `kind`
+// block epilogue: after the block's peer stores, the last block to finish raises flag `kind`. The
+// barrier orders the block's stores before thread 0's system fence (the cooperative-groups grid-sync
+// pattern); a fence in every thread made membar the top stall (profiles/r02_ncu_w2_group.txt).
 __device__ __forceinline__ void p2p_signal_last_block(const P2PArgs &a, int kind) {
-  __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence_system();
     const uint32_t t = atomicAdd(a.done + kind, 1u);
     if (t == gridDim.x - 1) {
       a.done[kind] = 0;

@@ -30,7 +30,7 @@ constexpr int POOL_THREADS = 256;
 // row of occurrence j. Direct mode (per-table sort path): g = base[t] + id validated here (R4) and the
 // occurrence's dY row index recorded for the backward; key mode (general sort path): g from the key
 // kernel. A row this rank owns is read from the table shard at local(g); at W > 1 a row owned by
-// another rank from the pulled rows at inv[j] (returned with REMOTE_BIT set).
+// another rank from the rows its owner pushed, at inv[j] (returned with REMOTE_BIT set).
 constexpr uint32_t REMOTE_BIT = 0x80000000u;
 template <bool REMOTE>
 __device__ __forceinline__ uint32_t pool_row_of(const PoolArgs &a, int64_t j, uint32_t slot, uint32_t orow) {

@@ -8,8 +8,8 @@
 //    (warp prefix in shared memory, tile prefix by a decoupled look-back over W counters, one lane per
 //    owner). A position's key then has rank `sendpos` among this rank's distinct keys of that owner
 //    (ascending g). Outputs: outidx per sorted position (the row of the merged gradient in the owner's
-//    region), inv per occurrence (the row the pull brings back), the head's local id into the owner's
-//    receive region (peer store) and into the local pull list. The last block publishes the per-owner
+//    region), inv per occurrence (the row the owner pushes back), the head's local id into the owner's
+//    receive region (peer store). The last block publishes the per-owner
 //    counts and this rank's input-error bits into every owner's xmat and raises KEYS.
 //  * k_merge_pass (A5): the owner receives W runs (source s at region s*cap), each sorted by local id;
 //    a stable merge tree (ceil(log2 W) passes of pairwise merge-path merges, ties keep the lower
@@ -55,11 +55,12 @@ __global__ void __launch_bounds__(RT_THREADS) k_route(const __grid_constant__ Ro
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t w0 = tile * RT_TILE + (int64_t)w * 32 * RT_ROWS;
-  uint32_t key[RT_ROWS];
+  uint32_t key[RT_ROWS], pay[RT_ROWS];  // (payloads loaded up front: pass 2's scattered stores need them)
 #pragma unroll
   for (int r = 0; r < RT_ROWS; ++r) {
     const int64_t p = w0 + r * 32 + lane;
     key[r] = p < a.n ? a.skey[p] : EMB_SENTINEL;
+    pay[r] = p < a.n ? a.spay[p] : 0u;
   }
   const uint32_t k_before = (lane == 0 && w0 > 0 && w0 - 1 < a.n) ? a.skey[w0 - 1] : EMB_SENTINEL;
   // head / owner of the lane's position in row r (warp-collective)
@@ -83,37 +84,45 @@ __global__ void __launch_bounds__(RT_THREADS) k_route(const __grid_constant__ Ro
     __syncwarp();
   }
   __syncthreads();
-  // ---- per owner: exclusive prefix over the warps, tile aggregate, look-back over earlier tiles
-  if (tid < W) {
-    const int o = tid;
-    uint32_t run = 0;
-    for (int q = 0; q < RT_WARPS; ++q) {
-      const uint32_t c = wcnt[q][o];
-      wcnt[q][o] = run;
-      run += c;
-    }
-    const uint32_t agg = run;
+  // ---- per owner (warp o): exclusive prefix over the warps, tile aggregate, decoupled look-back over
+  // earlier tiles, 32 predecessors per probe (tiles finish pass 1 at about the same time, so a
+  // one-tile-at-a-time walk would chain ~#tiles dependent L2 reads)
+  if (w < W) {
+    const int o = w;
+    const uint32_t c = lane < RT_WARPS ? wcnt[lane][o] : 0u;
+    const uint32_t incl = warp_incl_scan(c);
+    const uint32_t agg = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane < RT_WARPS) wcnt[lane][o] = incl - c;
     const unsigned long long tag = (unsigned long long)a.tag << 32;
     volatile unsigned long long *st = reinterpret_cast<volatile unsigned long long *>(a.status);
+    if (lane == 0) st[tile * P2P_MAXW + o] = tag | (tile == 0 ? LB_INC : LB_AGG) | agg;
     uint32_t excl = 0;
-    if (tile == 0) {
-      st[o] = tag | LB_INC | agg;
-    } else {
-      st[tile * P2P_MAXW + o] = tag | LB_AGG | agg;
+    if (tile > 0) {
       int64_t look = tile - 1;
       while (true) {
-        unsigned long long s;
-        do {
-          s = st[look * P2P_MAXW + o];
-        } while ((s >> 32) != a.tag || ((uint32_t)s & ~LB_VAL) == 0);
-        excl += (uint32_t)s & LB_VAL;
-        if ((uint32_t)s & LB_INC) break;
-        --look;
+        const int64_t t = look - lane;  // lane l probes tile look - l
+        unsigned long long sv = 0;
+        if (t >= 0) {
+          do {
+            sv = st[t * P2P_MAXW + o];
+          } while ((sv >> 32) != a.tag || ((uint32_t)sv & ~LB_VAL) == 0);
+        }
+        const bool inc = t < 0 || ((uint32_t)sv & LB_INC);
+        const uint32_t m = __ballot_sync(0xffffffffu, inc);
+        const int last = m ? __ffs(m) - 1 : 31;  // nearest inclusive predecessor ends the walk
+        uint32_t v = (lane <= last && t >= 0) ? ((uint32_t)sv & LB_VAL) : 0u;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        excl += v;
+        if (m) break;
+        look -= 32;
       }
-      st[tile * P2P_MAXW + o] = tag | LB_INC | (excl + agg);
+      if (lane == 0) st[tile * P2P_MAXW + o] = tag | LB_INC | (excl + agg);
     }
-    s_excl[o] = excl;
-    if (agg) atomicAdd(a.tot + o, agg);
+    if (lane == 0) {
+      s_excl[o] = excl;
+      if (agg) atomicAdd(a.tot + o, agg);
+    }
   }
   __syncthreads();
   // ---- pass 2: ranks, outputs, peer stores of the heads' local ids
@@ -135,12 +144,10 @@ __global__ void __launch_bounds__(RT_THREADS) k_route(const __grid_constant__ Ro
           bad = true;
         } else {
           sp = (uint32_t)pos;
-          a.inv[a.spay[p]] = (uint32_t)(o * cap + pos);
-          if (head) {
-            const uint32_t lk = local_of_g(key[r], a.ks);
-            a.send_local[o * cap + pos] = lk;
-            a.p2p.peer_recv_keys[o][(int64_t)parity_off * W * cap + (int64_t)a.p2p.rank * cap + pos] = lk;
-          }
+          a.inv[pay[r]] = (uint32_t)(o * cap + pos);
+          if (head)
+            a.p2p.peer_recv_keys[o][(int64_t)parity_off * W * cap + (int64_t)a.p2p.rank * cap + pos] =
+                local_of_g(key[r], a.ks);
         }
       }
       a.outidx[p] = sp;
@@ -150,14 +157,16 @@ __global__ void __launch_bounds__(RT_THREADS) k_route(const __grid_constant__ Ro
     __syncwarp();
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err, EMB_DEVERR_INTERNAL);
-  // ---- the last block publishes the counts + error bits and raises KEYS
-  __threadfence_system();
+  // ---- the last block publishes the counts + error bits and raises KEYS (one system fence per block,
+  // after the barrier: per-thread fences made membar the top stall, profiles/r02_ncu_w2_group.txt)
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(a.blk_done, 1u) == gridDim.x - 1;
+  if (tid == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(a.blk_done, 1u) == gridDim.x - 1;
+  }
   __syncthreads();
   if (!s_last) return;
   if (tid == 0) *a.blk_done = 0;
-  __threadfence();
   if (tid < W) {
     const int o = tid;
     const int64_t c = atomicExch(a.tot + o, 0u);
@@ -169,7 +178,6 @@ __global__ void __launch_bounds__(RT_THREADS) k_route(const __grid_constant__ Ro
     }
     a.p2p.peer_xmat[o][xmat_idx(a.p2p.epoch, 0, a.p2p.rank)] = c;
     a.p2p.peer_xmat[o][xmat_idx(a.p2p.epoch, 1, a.p2p.rank)] = eb;
-    __threadfence_system();
   }
   __syncthreads();
   if (tid == 0) p2p_raise(a.p2p, P2P_KEYS);

@@ -28,7 +28,7 @@ SHARD = {"cyclic": 0, "block": 1}
 # every symbol include/emb.h declares (checked by tests/test_abi.py)
 EXPORTED = [
     "emb_create", "emb_create_group", "emb_destroy", "emb_get_unique_id", "emb_lookup", "emb_lookup_prefetch",
-    "emb_backward_update", "emb_lookup_group", "emb_backward_update_group", "emb_lookup_host",
+    "emb_backward_update", "emb_lookup_group", "emb_backward_update_group", "emb_lookup_host", "emb_host_sync",
     "emb_backward_update_host", "emb_read_rows", "emb_write_rows", "emb_last_step_info", "emb_last_unique",
     "emb_last_owner_unique", "emb_rows_local", "emb_profile_enable", "emb_profile_reset", "emb_profile_read",
     "emb_profile_name", "emb_clear_error", "emb_last_error",
@@ -91,6 +91,7 @@ def lib() -> ctypes.CDLL:
     L.emb_backward_update.argtypes = [vp, vp, ctypes.c_double, vp]
     L.emb_lookup_host.argtypes = [vp, vp, vp, i32, i64, vp, vp]
     L.emb_backward_update_host.argtypes = [vp, vp, ctypes.c_double, vp]
+    L.emb_host_sync.argtypes = [vp]
     L.emb_read_rows.argtypes = [vp, i32, vp, i64, vp, vp]
     L.emb_write_rows.argtypes = [vp, i32, vp, i64, vp, vp]
     L.emb_last_step_info.argtypes = [vp, ctypes.POINTER(StepInfoC)]
@@ -226,6 +227,10 @@ class EmbeddingLayer:
     def backward_update_host(self, d_out: np.ndarray, lr: float, stream=None):
         self._check(lib().emb_backward_update_host(self.h, _ptr(d_out), float(lr), _stream(stream, self.device)),
                     "emb_backward_update_host")
+
+    def host_sync(self):
+        """Wait for every host-buffer call (asynchronous: the buffers must stay untouched until then)."""
+        self._check(lib().emb_host_sync(self.h), "emb_host_sync")
 
     # ---- host-synchronous helpers
     def read_rows(self, table: int, rows) -> Tuple[np.ndarray, np.ndarray]:

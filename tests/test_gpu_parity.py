@@ -377,20 +377,29 @@ def test_read_write_rows_roundtrip_bitwise(torch):
 
 
 def test_host_buffer_path(torch):
+    """The asynchronous host-buffer entry points (double-buffered staging, H2D / D2H copy streams): four
+    steps enqueued back to back with no synchronisation in between (each step's pinned buffers kept
+    alive), then emb_host_sync; every step's Y and the final rows match the free-running oracle."""
     wl = synthgen.WORKLOADS["C1"].with_(ids="zipf", zipf_s=1.2, opt="adagrad")
     cfg = O.config_from_workload(wl)
-    bt = synthgen.make_batch(wl, batch=256)
-    layer = _layer(wl, 256, bt.nnz)
+    bts = [synthgen.make_batch(wl, step=k, batch=256) for k in range(4)]
+    layer = _layer(wl, 256, max(bt.nnz for bt in bts))
     ora = O.OracleEmbedding(cfg)
     try:
-        out = np.empty((256, wl.num_slots, wl.dim), np.float32)
-        layer.lookup_host(bt.ids, bt.offsets, 256, bt.nnz, out)
-        layer.backward_update_host(bt.dy, 0.05)
-        (Yo,) = ora.lookup([(bt.ids, bt.offsets, 256)])
-        ora.backward_update([bt.dy], 0.05)
-        _check_close(out, Yo, "Y host path")
-        g = _touched_rows(cfg, bt)
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        ins = [(pin(bt.ids), pin(bt.offsets), pin(bt.dy)) for bt in bts]
+        outs = [torch.empty((256, wl.num_slots, wl.dim), dtype=torch.float32).pin_memory() for _ in bts]
+        for (i_, o_, d_), out, bt in zip(ins, outs, bts):
+            layer.lookup_host(i_.numpy(), o_.numpy(), 256, bt.nnz, out.numpy())
+            layer.backward_update_host(d_.numpy(), 0.05)
+        layer.host_sync()
+        for k, bt in enumerate(bts):
+            (Yo,) = ora.lookup([(bt.ids, bt.offsets, 256)])
+            ora.backward_update([bt.dy], 0.05)
+            _check_close(outs[k].numpy(), Yo, f"Y host path step {k}")
+        g = np.unique(np.concatenate([_touched_rows(cfg, bt) for bt in bts]))
         w, a = _read_global(layer, cfg, g)
         _check_close(w, ora.rows(g)[0], "w host path")
+        _check_close(a, ora.rows(g)[1], "a host path")
     finally:
         layer.close()
