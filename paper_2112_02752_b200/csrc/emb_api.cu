@@ -483,8 +483,8 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
   } else if (W > 1) {
     h->cap = group_cap;
   }
-  if (W > 1 && (int64_t)W * h->cap >= (1ll << 31) - 1)
-    return fail(h, EMB_ERR_INVALID, "world * max_ids must be < 2^31 - 1");
+  if (W > 1 && ((int64_t)W * h->cap >= (1ll << 31) - 1 || h->cap > (int64_t)OUT_POS_MASK))
+    return fail(h, EMB_ERR_INVALID, "world > 1 needs world * max_ids < 2^31 - 1 and max_ids < 2^28");
 
   // table shard + state
   const size_t row_elems = (size_t)std::max<int64_t>(h->rows_local, 1) * h->D;
@@ -610,9 +610,11 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
       gslot.push_back(h->S);
       h->G = (int32_t)gbase.size();
       // key ranges (CTAs) per group: ~4K occurrences per CTA at the capacity bound (K sweep on C2:
-      // K=2/4/8/16 -> 206/157/176/201 us per step); every CTA scans its whole group, so K stays small
+      // K=2/4/8/16 -> 206/157/176/201 us per step); every CTA scans its whole group, so K stays small.
+      // With few groups (C1: one table) the CTAs would not fill the GPU: ~1K occurrences per CTA then
       const int64_t per = (h->max_ids + h->G - 1) / h->G;
-      h->segK = (int32_t)std::min<int64_t>(16, std::max<int64_t>(1, (per + 4095) / 4096));
+      const int64_t per_cta = h->G >= 8 ? 4096 : 1024;
+      h->segK = (int32_t)std::min<int64_t>(16, std::max<int64_t>(1, (per + per_cta - 1) / per_cta));
       if (const char *ek = getenv("EMB_SEGK")) h->segK = std::max(1, std::min(32, atoi(ek)));  // experiment knob
       if (dalloc(h, &h->run_k, h->max_ids) || dalloc(h, &h->run_i, h->max_ids))
         return fail(h, EMB_ERR_NOMEM, "alloc sort runs");

@@ -79,15 +79,32 @@ __device__ __forceinline__ void stg_frag(float *p, const VecF<CPL> &v) {
 }
 
 // optimizer constants, converted once per kernel
+// PRECISE (template parameter of the Adagrad sinks, chosen on the host for lr > 1): fp64 from the fp32
+// state, the oracle's formula with one rounding each, instead of R16' (fp32 FMA accumulator +
+// approximate sqrt / reciprocal, whose absolute error ~lr * 3e-7 exceeds the 1e-6 absolute tolerance
+// once lr > ~3). A separate instantiation: a runtime branch, even out of line, cost the fast path
+// 79 -> 125 us at C2 (register pressure around the call), DESIGN.md §2 R16'.
 struct OptConst {
-  double lr;
+  double lr, eps;
   float lrf, epsf;
 };
-__device__ __forceinline__ OptConst opt_const(const GradArgs &a) { return {a.lr, (float)a.lr, (float)a.eps}; }
+__device__ __forceinline__ OptConst opt_const(const GradArgs &a) { return {a.lr, a.eps, (float)a.lr, (float)a.eps}; }
+
+// the fp64 Adagrad sink of one lane's fragment (PRECISE instantiations only)
+template <int CPL>
+__device__ __forceinline__ void adagrad_precise(const double (&acc)[CPL], const VecF<CPL> &wv, const VecF<CPL> &av,
+                                             VecF<CPL> &wo, VecF<CPL> &ao, double lr, double eps) {
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const double an = __dadd_rn((double)av.v[c], __dmul_rn(acc[c], acc[c]));
+    ao.v[c] = (float)an;
+    wo.v[c] = (float)__dsub_rn((double)wv.v[c], __ddiv_rn(__dmul_rn(lr, acc[c]), __dadd_rn(__dsqrt_rn(an), eps)));
+  }
+}
 
 // optimizer update (MODE 0/1) of one lane's row fragment, w / a already in registers; D = row width
 // (compile-time when DC != 0)
-template <int CPL, int MODE>
+template <int CPL, int MODE, bool PRECISE = false>
 __device__ __forceinline__ void apply_frag(const GradArgs &a, const OptConst &oc, const double (&acc)[CPL],
                                            const VecF<CPL> &wv, const VecF<CPL> &av, size_t row_off) {
   VecF<CPL> wo;
@@ -97,22 +114,48 @@ __device__ __forceinline__ void apply_frag(const GradArgs &a, const OptConst &oc
     stg_frag<CPL>(a.w + row_off, wo);
   } else {
     VecF<CPL> ao;
+    if constexpr (PRECISE) {
+      adagrad_precise<CPL>(acc, wv, av, wo, ao, oc.lr, oc.eps);
+    } else {
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const float g = (float)acc[c];
-      const float af = __fmaf_rn(g, g, av.v[c]);  // a + G^2: one fp32 FMA from the rounded G (R16')
-      const float r = rcp_approx(sqrt_approx(af) + oc.epsf);
-      ao.v[c] = af;
-      wo.v[c] = wv.v[c] - (oc.lrf * g) * r;
+      for (int c = 0; c < CPL; ++c) {
+        const float g = (float)acc[c];
+        const float af = __fmaf_rn(g, g, av.v[c]);  // a + G^2: one fp32 FMA from the rounded G (R16')
+        const float r = rcp_approx(sqrt_approx(af) + oc.epsf);
+        ao.v[c] = af;
+        wo.v[c] = wv.v[c] - (oc.lrf * g) * r;
+      }
     }
     stg_frag<CPL>(a.w + row_off, wo);
     stg_frag<CPL>(a.a + row_off, ao);
   }
 }
 
+// fp64 row-wise Adagrad sink (PRECISE instantiations only): warp-collective
+template <int CPL>
+__device__ __forceinline__ void rowwise_precise(const GradArgs &a, const OptConst &oc, const double (&acc)[CPL],
+                                             const VecF<CPL> &wv, float a_old, size_t row_off, uint32_t lrow,
+                                             bool active, int D) {
+  double sd = 0.0;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+    if (active) sd = __dadd_rn(sd, __dmul_rn(acc[c], acc[c]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sd = __dadd_rn(sd, __shfl_xor_sync(0xffffffffu, sd, o));
+  const double an = __dadd_rn((double)a_old, __ddiv_rn(sd, (double)D));
+  const double den = __dadd_rn(__dsqrt_rn(an), oc.eps);
+  if (active) {
+    VecF<CPL> wo;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) wo.v[c] = (float)__dsub_rn((double)wv.v[c], __ddiv_rn(__dmul_rn(oc.lr, acc[c]), den));
+    stg_frag<CPL>(a.w + row_off, wo);
+  }
+  if ((threadIdx.x & 31) == 0) a.a[lrow] = (float)an;
+}
+
 // row-wise Adagrad (MODE 4) of one row: warp-collective (every lane calls it; inactive lanes hold no
 // columns). a_old is the row's accumulator (the same value in every lane).
-template <int CPL>
+template <int CPL, bool PRECISE = false>
 __device__ __forceinline__ void apply_rowwise(const GradArgs &a, const OptConst &oc, const double (&acc)[CPL],
                                               const VecF<CPL> &wv, float a_old, size_t row_off, uint32_t lrow,
                                               bool active, int D) {
@@ -121,6 +164,10 @@ __device__ __forceinline__ void apply_rowwise(const GradArgs &a, const OptConst 
   // (commutative), so all lanes end with the bitwise identical total. Relative error <= ~4e-7 against
   // the oracle's fp64 mean of G^2 (reading R14'); the fp64 chain cost ~20 us of the C2 step.
   VecF<CPL> g;
+  if constexpr (PRECISE) {  // fp64 from the fp32 state (see OptConst)
+    rowwise_precise<CPL>(a, oc, acc, wv, a_old, row_off, lrow, active, D);
+    return;
+  }
   float s = 0.f;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
@@ -145,9 +192,10 @@ __device__ __forceinline__ void apply_rowwise(const GradArgs &a, const OptConst 
 // destination row of a merged per-key gradient (MODE 3, requester side at W > 1): the owner o of key g
 // holds a region of cap rows per source; this rank's key of rank ui in o's list goes to row
 // rank*cap + ui there (peer memory over NVLink, or this rank's own buffer when o == rank)
-__device__ __forceinline__ float *out_row3(const GradArgs &a, uint32_t key, uint32_t ui, int D) {
-  const uint32_t o = owner_of_g(key, a.ks);
-  return a.p2p.peer_grecv[o] + (size_t)((int64_t)a.p2p.rank * a.p2p.cap + ui) * (2 * D);  // (hi/lo rows)
+__device__ __forceinline__ float *out_row3(const GradArgs &a, uint32_t ui, int D) {
+  // ui = owner << OUT_OWNER_SHIFT | rank in the owner's list (written by k_route)
+  return a.p2p.peer_grecv[ui >> OUT_OWNER_SHIFT] +
+         (size_t)((int64_t)a.p2p.rank * a.p2p.cap + (ui & OUT_POS_MASK)) * (2 * D);  // (hi/lo rows)
 }
 
 // a merged per-key partial crosses the exchange as a double-float pair: hi = fp32(G), lo = fp32(G - hi)
@@ -226,7 +274,7 @@ __device__ int64_t seg_bound_warp(const uint32_t *skey, int64_t n, int64_t p, ui
 
 // piece crossing a range boundary: store the partial, take a ticket on the segment; the last arriving
 // warp sums the partials in warp order and sinks the total. (Rare path: <= 2 per warp; not inlined.)
-template <int CPL, int MODE>
+template <int CPL, int MODE, bool PRECISE>
 __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, int64_t slot, int64_t pos,
                                         uint32_t key, int64_t R, int64_t n) {
   const int lane = threadIdx.x & 31;
@@ -269,7 +317,7 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
     }
   }
   if constexpr (MODE == 3) {
-    store_hilo<CPL>(out_row3(a, key, a.useg[pos], D) + 2 * col, tot);
+    store_hilo<CPL>(out_row3(a, a.useg[pos], D) + 2 * col, tot);
   } else if constexpr (MODE == 4) {
     const uint32_t lrow = key & a.lmask;
     const size_t off = (size_t)lrow * D + col;
@@ -277,13 +325,13 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
     if (active) ldg_frag<CPL>(wv, a.w + off);
     else wv.zero();
     const float a_old = __ldcg(a.a + lrow);
-    apply_rowwise<CPL>(a, opt_const(a), tot, wv, a_old, off, lrow, active, D);
+    apply_rowwise<CPL, PRECISE>(a, opt_const(a), tot, wv, a_old, off, lrow, active, D);
   } else {
     const size_t off = (size_t)(key & a.lmask) * D + col;
     VecF<CPL> wv, av;
     ldg_frag<CPL>(wv, a.w + off);
     if (MODE == 1) ldg_frag<CPL>(av, a.a + off);
-    apply_frag<CPL, MODE>(a, opt_const(a), tot, wv, av, off);
+    apply_frag<CPL, MODE, PRECISE>(a, opt_const(a), tot, wv, av, off);
   }
 }
 
@@ -295,7 +343,7 @@ struct TileMeta {
   uint32_t vmask, hmask, tmask;  // warp-uniform: valid / head / tail
 };
 
-template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2, bool LO = false>
+template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2, bool LO = false, bool PRECISE = false>
 __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ GradArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   // row arrays per stage: contribution (+ its low part, LO: owner side at W > 1), w, a
@@ -364,7 +412,7 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
       if (SINK_OPT && (int64_t)(k & a.lmask) >= a.nrows) bad = true;
       if (!SINK_OPT) {
         uo = uo_in;
-        if ((int64_t)uo >= a.nout) bad = true;
+        if ((int64_t)(uo & OUT_POS_MASK) >= a.nout || (uo >> OUT_OWNER_SHIFT) >= (uint32_t)a.p2p.world) bad = true;
       }
     }
     uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
@@ -489,7 +537,7 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
           if (begins) {  // complete inside the range
             if constexpr (!SINK_OPT) {
               const uint32_t ui = __shfl_sync(0xffffffffu, m.uo, i);
-              if (active) store_hilo<CPL>(out_row3(a, ki, ui, D) + 2 * col, acc.v);
+              if (active) store_hilo<CPL>(out_row3(a, ui, D) + 2 * col, acc.v);
             } else if constexpr (MODE == 4) {
               VecF<CPL> wv;
               if (active) lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((OFF_W + i) * D));
@@ -498,17 +546,17 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
               const uint32_t sa_ = wbase + (uint32_t)(s * stage_floats * 4) + 4u * (uint32_t)(OFF_A * D + i);
               asm volatile("ld.shared.f32 %0, [%1];" : "=f"(a_old) : "r"(sa_));
               const uint32_t lrow = ki & a.lmask;
-              apply_rowwise<CPL>(a, oc, acc.v, wv, a_old, (size_t)lrow * D + col, lrow, active, D);
+              apply_rowwise<CPL, PRECISE>(a, oc, acc.v, wv, a_old, (size_t)lrow * D + col, lrow, active, D);
             } else {
               if (active) {
                 VecF<CPL> wv, av;
                 lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((OFF_W + i) * D));
                 if (MODE == 1) lds_frag<CPL>(av, sbase + 4u * (uint32_t)((OFF_A + i) * D));
-                apply_frag<CPL, MODE>(a, oc, acc.v, wv, av, (size_t)(ki & a.lmask) * D + col);
+                apply_frag<CPL, MODE, PRECISE>(a, oc, acc.v, wv, av, (size_t)(ki & a.lmask) * D + col);
               }
             }
           } else {
-            span_piece<CPL, MODE>(a, acc, 2 * gw, t0 + i, ki, R, n);  // continuation piece that ends here
+            span_piece<CPL, MODE, PRECISE>(a, acc, 2 * gw, t0 + i, ki, R, n);  // continuation piece that ends here
           }
 #pragma unroll
           for (int c = 0; c < CPL; ++c) acc.v[c] = 0.0;
@@ -541,14 +589,14 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
     }
   }
   cp_async_wait<0>();
-  if (open && !broken) span_piece<CPL, MODE>(a, acc, begins ? 2 * gw + 1 : 2 * gw, open_pos, open_key, R, n);  // continues past the range
+  if (open && !broken) span_piece<CPL, MODE, PRECISE>(a, acc, begins ? 2 * gw + 1 : 2 * gw, open_pos, open_key, R, n);  // continues past the range
   }  // p_lo < p_hi
   if (a.signal_kind >= 0) grad_signal_last_cta(a);
 }
 
 static int g_sms = 0;
 
-template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2, bool LO = false>
+template <int CPL, int T, int NS, bool MEAN, int MODE, int DC, int MINB = 2, bool LO = false, bool PRECISE = false>
 static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
   constexpr int NA = ((MODE == 1) ? 3 : ((MODE == 0 || MODE == 4) ? 2 : 1)) + (LO ? 1 : 0);
   const size_t per_warp = (size_t)NS * ((size_t)NA * T * a.dim + (MODE == 4 ? T : 0)) * sizeof(float);
@@ -562,18 +610,18 @@ static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
   if (dev < 0 || dev >= EMB_MAX_DEVICES) return cudaErrorInvalidDevice;
   if (attr[dev] < smem) {
     cudaError_t e =
-        cudaFuncSetAttribute(k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO, PRECISE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr[dev] = smem;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO>, wpc * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO, PRECISE>, wpc * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)g_sms * per_sm;
   const int64_t max_blocks = ((a.n + 4 * T - 1) / (4 * T) + wpc - 1) / wpc;  // >= 4 tiles per warp
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO><<<(unsigned)blocks, wpc * 32, smem, st>>>(a);
+  k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO, PRECISE><<<(unsigned)blocks, wpc * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -599,6 +647,21 @@ static cudaError_t launch_grad_d(const GradArgs &a, cudaStream_t st) {
   return launch_grad_t<CPL, T, 2, false, 3, DC>(a, st);
 }
 
+template <int CPL, int T>
+static cudaError_t launch_grad_precise(const GradArgs &a, int mode, cudaStream_t st) {
+  const bool mean = a.blen != nullptr;
+  if (a.src_lo) {
+    if (mode == 1) return launch_grad_t<CPL, T, 2, false, 1, 0, 2, true, true>(a, st);
+    return launch_grad_t<CPL, T, 2, false, 4, 0, 2, true, true>(a, st);
+  }
+  if (mean) {
+    if (mode == 1) return launch_grad_t<CPL, T, 2, true, 1, 0, 2, false, true>(a, st);
+    return launch_grad_t<CPL, T, 2, true, 4, 0, 2, false, true>(a, st);
+  }
+  if (mode == 1) return launch_grad_t<CPL, T, 2, false, 1, 0, 2, false, true>(a, st);
+  return launch_grad_t<CPL, T, 2, false, 4, 0, 2, false, true>(a, st);
+}
+
 int64_t grad_max_warps(int dev) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -612,16 +675,11 @@ cudaError_t launch_grad(const GradArgs &a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  if (a.dim == 64 && a.blen == nullptr && a.sink_mode == 0 && a.opt == 1) {
-    static int var = -1;  // experiment knob for the C2 path: tile size x register cap
-    if (var < 0) {
-      const char *v = getenv("EMB_GRAD_VAR");
-      var = v ? atoi(v) : 0;
-    }
-    if (var == 1) return launch_grad_t<2, 4, 2, false, 1, 64, 3>(a, st);
-    if (var == 2) return launch_grad_t<2, 8, 2, false, 1, 64, 3>(a, st);
-    if (var == 3) return launch_grad_t<2, 16, 2, false, 1, 64, 1>(a, st);
-    if (var == 4) return launch_grad_t<2, 4, 2, false, 1, 64, 4>(a, st);
+  const int mode = a.sink_mode == 2 ? 3 : (a.opt == 1 ? 1 : (a.opt == 2 ? 4 : 0));
+  if ((mode == 1 || mode == 4) && a.lr > 1.0) {  // fp64 Adagrad sinks (OptConst): generic-D kernels
+    if (a.dim <= 64) return launch_grad_precise<2, 8>(a, mode, st);
+    if (a.dim <= 128) return launch_grad_precise<4, 8>(a, mode, st);
+    return launch_grad_precise<8, 8>(a, mode, st);
   }
   if (a.dim == 64) return launch_grad_d<2, 8, 64>(a, st);
   if (a.dim == 128) return launch_grad_d<4, 8, 128>(a, st);

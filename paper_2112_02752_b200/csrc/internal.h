@@ -91,12 +91,15 @@ cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t 
 // stored straight into owner o's receive region; per sorted position outidx = sendpos; per
 // occurrence inv = o*cap + sendpos (the row owner o pushes back). The last block publishes the
 // per-owner counts and this rank's input-error bits into every owner's xmat and raises KEYS.
+// outidx of a sorted position: owner << OUT_OWNER_SHIFT | rank in that owner's list (cap < 2^28)
+constexpr uint32_t OUT_OWNER_SHIFT = 28;
+constexpr uint32_t OUT_POS_MASK = (1u << OUT_OWNER_SHIFT) - 1u;
 struct RouteArgs {
   const uint32_t *skey, *spay;
   int64_t n;
   KeySpace ks;
   P2PArgs p2p;
-  uint32_t *outidx;       // [n]
+  uint32_t *outidx;       // [n] owner << OUT_OWNER_SHIFT | sendpos
   uint32_t *inv;          // [max_ids] by occurrence
   int64_t *scnt;          // [P2P_MAXW] out
   uint32_t *tot;          // [P2P_MAXW] zero on entry, left zero
@@ -167,6 +170,7 @@ struct PoolArgs {
   const float *rows_remote;  // W > 1: rows pushed by their owners [W*cap][D]
   int64_t nrows_remote;      // W * cap (bounds guard)
   const uint32_t *row_idx; // W > 1: inv (occurrence -> o*cap + sendpos) for rows owned elsewhere
+  int32_t bags_per_tile;   // 32 or 8 bags per warp tile (launch_pool sets it)
   float *out;
   uint32_t *err;           // device error word
   uint32_t *err_host;      // mapped pinned host word

@@ -145,7 +145,7 @@ __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, in
   while (cb < nbt) flush();
 }
 
-template <int CPL, int RCH, int MINB, bool REMOTE>
+template <int CPL, int RCH, int MINB, bool REMOTE, int BPT>
 __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_constant__ PoolArgs a) {
   // RCH rows per batch of the single-id path (RCH * CPL floats in flight per lane)
   const int lane = threadIdx.x & 31;
@@ -154,12 +154,13 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
   const bool active = col < D;
   const uint32_t B = (uint32_t)a.batch, S = (uint32_t)a.num_slots;
   const int64_t nb = (int64_t)a.num_slots * a.batch;
-  const int64_t ntiles = (nb + 31) / 32;
+  constexpr int bpt = BPT;  // bags per warp tile
+  const int64_t ntiles = (nb + bpt - 1) / bpt;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t tile = gw; tile < ntiles; tile += nwarps) {
-    const int64_t b0 = tile * 32;
-    const int nbt = (int)((nb - b0) < 32 ? (nb - b0) : 32);
+    const int64_t b0 = tile * bpt;
+    const int nbt = (int)((nb - b0) < bpt ? (nb - b0) : bpt);
     const bool inb = lane < nbt;
     const uint32_t bag = (uint32_t)b0 + lane;
     int64_t off = 0, offn = 0;
@@ -220,10 +221,14 @@ static cudaError_t launch_pool_t(const PoolArgs &a, int64_t ntiles, cudaStream_t
   // one tile per warp (not persistent), so the concurrent side-stream sort CTAs get SMs as soon as
   // they are ready and the pool fills the rest
   const int64_t blocks = (ntiles * 32 + POOL_THREADS - 1) / POOL_THREADS;
-  if (a.ks.world > 1)
-    k_pool<CPL, RCH, MINB, true><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
-  else
-    k_pool<CPL, RCH, MINB, false><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
+  const bool remote = a.ks.world > 1;
+  if (a.bags_per_tile == 32) {
+    if (remote) k_pool<CPL, RCH, MINB, true, 32><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
+    else k_pool<CPL, RCH, MINB, false, 32><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
+  } else {
+    if (remote) k_pool<CPL, RCH, MINB, true, 8><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
+    else k_pool<CPL, RCH, MINB, false, 8><<<(unsigned)blocks, POOL_THREADS, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 
@@ -236,10 +241,14 @@ cudaError_t launch_publish_err(const uint32_t *err, uint32_t *err_host, cudaStre
   return cudaGetLastError();
 }
 
-cudaError_t launch_pool(const PoolArgs &a, cudaStream_t st) {
-  const int64_t nb = (int64_t)a.num_slots * a.batch;
+cudaError_t launch_pool(const PoolArgs &a0, cudaStream_t st) {
+  const int64_t nb = (int64_t)a0.num_slots * a0.batch;
   if (nb == 0) return cudaSuccess;
-  const int64_t ntiles = (nb + 31) / 32;
+  PoolArgs a = a0;
+  // bags per warp tile: 32 (one per lane) fills the GPU once there are >= ~150K bags; small batches
+  // (C1: 4,096 bags, 128 tiles) get 8 per tile so 4x more warps walk their occurrences in parallel
+  a.bags_per_tile = nb >= 148 * 8 * 32 * 4 ? 32 : 8;
+  const int64_t ntiles = (nb + a.bags_per_tile - 1) / a.bags_per_tile;
   // D <= 64: all 32 rows of a tile in flight per lane (registers allow it because the loads are
   // unconditional): C2 step 136.6 -> 133.5 us against 16 rows (round 1)
   if (a.dim <= 64) return launch_pool_t<2, 32, 3>(a, ntiles, st);

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route(const __grid_constant__ Ro
         if (pos < 0 || pos >= cap) {
           bad = true;
         } else {
-          sp = (uint32_t)pos;
+          sp = (o << OUT_OWNER_SHIFT) | (uint32_t)pos;  // owner in the top bits (no division downstream)
           a.inv[pay[r]] = (uint32_t)(o * cap + pos);
           if (head)
             a.p2p.peer_recv_keys[o][(int64_t)parity_off * W * cap + (int64_t)a.p2p.rank * cap + pos] =

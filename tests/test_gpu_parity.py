@@ -403,3 +403,44 @@ def test_host_buffer_path(torch):
         _check_close(a, ora.rows(g)[1], "a host path")
     finally:
         layer.close()
+
+
+@pytest.mark.parametrize("opt", ["adagrad", "rowwise_adagrad"])
+@pytest.mark.parametrize("lr", [1.0, 10.0])
+def test_adagrad_large_lr_extreme_values(torch, opt, lr):
+    """Reading R16' at its limits: learning rates 1 (fast fp32 sink: sqrt/rcp approximations, error
+    <= ~lr*3e-7) and 10 (the fp64 sink, switched on for lr > 1), with huge merged gradients (|G| ~ 1e4),
+    subnormal ones (dY ~ 1e-40), accumulators far above 1 (a = 1e6) and near 0, and weights near 0 --
+    against the oracle within the contract tolerance, two resynced steps."""
+    wl = synthgen.WORKLOADS["C1"].with_(rows=(64,), slot_table=(0, 0), dim=16, opt=opt, init_accum=0.0)
+    cfg = O.config_from_workload(wl)
+    layer = _layer(wl, 64, 128)
+    ora = O.OracleEmbedding(cfg)
+    rng = np.random.default_rng(7)
+    try:
+        rows = np.arange(64)
+        w0 = (rng.standard_normal((64, 16)) * 1e-3).astype(np.float32)
+        aw = 16 if opt == "adagrad" else 1
+        a0 = np.where(np.arange(64)[:, None] % 3 == 0, 1e6, np.where(np.arange(64)[:, None] % 3 == 1, 1e-30, 0.5))
+        a0 = np.broadcast_to(a0, (64, aw)).astype(np.float32).copy()
+        layer.write_rows(0, rows, w0, a0)
+        for step in range(2):
+            ids = np.concatenate([np.arange(64), rng.integers(0, 8, 64)])  # slot 0: every row; slot 1: hot rows
+            offs = np.arange(129)
+            dy = np.empty((64, 2, 16), np.float32)
+            scale = np.where(np.arange(64) % 4 == 0, 1e4, np.where(np.arange(64) % 4 == 1, 1e-40, 1.0))
+            dy[:, 0, :] = (rng.standard_normal((64, 16)) * scale[:, None]).astype(np.float32)
+            dy[:, 1, :] = rng.standard_normal((64, 16)).astype(np.float32)
+            bt = synthgen.Batch(ids=ids.astype(np.int64), offsets=offs.astype(np.int64), batch=64, dy=dy)
+            w, a = _read_global(layer, cfg, rows)
+            ora.load_rows(rows, w, a)
+            Y, *_ = _run_step(torch, layer, bt, lr)
+            (Yo,) = ora.lookup([(bt.ids, bt.offsets, 64)])
+            _check_close(Y, Yo, f"Y step {step}")
+            ora.backward_update([bt.dy], lr)
+            w, a = _read_global(layer, cfg, rows)
+            wo, ao = ora.rows(rows)
+            _check_close(w, wo, f"w step {step} lr {lr}")
+            _check_close(a, ao, f"a step {step} lr {lr}")
+    finally:
+        layer.close()

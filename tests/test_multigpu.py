@@ -41,5 +41,9 @@ def test_two_gpu_row_sharded_parity(case, shard):
     env = dict(os.environ, EMB_MGPU_CASE=case, EMB_MGPU_SHARD=shard)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tests", "mgpu_worker.py")]
-    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    for _ in range(3):  # a fresh port per attempt: the rendezvous port can be taken between probe and bind
+        cmd[cmd.index("--master-port") + 1] = str(_port())
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+        if "EADDRINUSE" not in r.stderr:
+            break
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
