@@ -552,7 +552,10 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
     bad |= dalloc(h, &h->route_tot, P2P_MAXW) != cudaSuccess;
     bad |= dalloc(h, &h->route_counter, 1) != cudaSuccess;
     bad |= dalloc(h, &h->route_done, 1) != cudaSuccess;
-    bad |= dalloc(h, &h->route_status, route_status_words(N)) != cudaSuccess;
+    // look-back words: one set per route tile, or per sort CTA when the route is fused into the
+    // per-table sort (groups x ranges <= EMB_MAX_SLOTS x 32)
+    bad |= dalloc(h, &h->route_status, std::max<size_t>(route_status_words(N), (size_t)(EMB_MAX_SLOTS * 32 + 1) * P2P_MAXW)) !=
+           cudaSuccess;
     bad |= dalloc(h, &h->recv_keys, 2 * WC) != cudaSuccess;
     bad |= dalloc(h, &h->uniq_rows, (size_t)WC * h->D) != cudaSuccess;
     bad |= dalloc(h, &h->grecv, (size_t)2 * WC * h->D) != cudaSuccess;  // hi and lo parts
@@ -638,7 +641,8 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
     CUDA_TRY(h, cudaMemset(h->route_tot, 0, sizeof(uint32_t) * P2P_MAXW));
     CUDA_TRY(h, cudaMemset(h->route_counter, 0, sizeof(uint32_t)));
     CUDA_TRY(h, cudaMemset(h->route_done, 0, sizeof(uint32_t)));
-    CUDA_TRY(h, cudaMemset(h->route_status, 0, sizeof(uint64_t) * route_status_words(N)));
+    CUDA_TRY(h, cudaMemset(h->route_status, 0,
+                           sizeof(uint64_t) * std::max<size_t>(route_status_words(N), (size_t)(EMB_MAX_SLOTS * 32 + 1) * P2P_MAXW)));
     CUDA_TRY(h, cudaMemset(h->scnt, 0, sizeof(int64_t) * P2P_MAXW));
     CUDA_TRY(h, cudaMemset(h->n_merged, 0, sizeof(int64_t)));
     CUDA_TRY(h, cudaMemset(h->xmat, 0, sizeof(int64_t) * 4 * P2P_MAXW));
@@ -853,22 +857,6 @@ emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
   h->p2p.epoch = h->epoch;
   h->skey = h->k0;
   h->spay = h->v0;
-  if (batch > 0 && nnz > 0) {
-    if (h->segsort_ok) {
-      SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, 0);
-      sa.validate = 1;
-      LAUNCH(h, KID_SORT_PASS, st, launch_segsort(sa, h->G, st));
-    } else {
-      LAUNCH(h, KID_KEYS, st, launch_keys(keys_args(h, ids, offsets, batch, nnz), st));
-      int nl = 0;
-      cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz, h->ks.key_bits,
-                                       st, &h->skey, &h->spay, &nl, prof_hook, h);
-      if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
-      h->launches += nl;
-    }
-  } else if (batch > 0 && !h->segsort_ok) {
-    LAUNCH(h, KID_KEYS, st, launch_keys(keys_args(h, ids, offsets, batch, nnz), st));  // validates the CSR
-  }
   RouteArgs ra{};
   ra.skey = h->skey;
   ra.spay = h->spay;
@@ -886,6 +874,32 @@ emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
   ra.tag = h->route_tag;
   ra.err = h->err_dev;
   ra.extra_err = h->step_err_bits;
+  static int fuse = -1;  // experiment knob EMB_FUSED_ROUTE=0: separate k_route after the per-table sort
+  if (fuse < 0) fuse = getenv("EMB_FUSED_ROUTE") ? atoi(getenv("EMB_FUSED_ROUTE")) : 1;
+  if (batch > 0 && nnz > 0) {
+    if (h->segsort_ok) {
+      SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, 0);
+      sa.validate = 1;
+      if (fuse) {  // the route runs in the sort's epilogue (no separate launch)
+        sa.route = 1;
+        sa.rt = ra;
+        LAUNCH(h, KID_SORT_PASS, st, launch_segsort(sa, h->G, st));
+        return EMB_OK;
+      }
+      LAUNCH(h, KID_SORT_PASS, st, launch_segsort(sa, h->G, st));
+    } else {
+      LAUNCH(h, KID_KEYS, st, launch_keys(keys_args(h, ids, offsets, batch, nnz), st));
+      int nl = 0;
+      cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz, h->ks.key_bits,
+                                       st, &h->skey, &h->spay, &nl, prof_hook, h);
+      if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+      h->launches += nl;
+      ra.skey = h->skey;
+      ra.spay = h->spay;
+    }
+  } else if (batch > 0 && !h->segsort_ok) {
+    LAUNCH(h, KID_KEYS, st, launch_keys(keys_args(h, ids, offsets, batch, nnz), st));  // validates the CSR
+  }
   LAUNCH(h, KID_ROUTE, st, launch_route(ra, st));
   return EMB_OK;
 }

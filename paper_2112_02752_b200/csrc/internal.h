@@ -265,6 +265,8 @@ struct SegSortArgs {
   uint32_t *run_k, *run_i;  // [nnz] sorted runs (local key, chunk-relative index)
   int32_t K;                // chunks (CTAs) per group
   int32_t validate;         // check the CSR offsets + fill uncovered positions (W > 1; the pool does it at W = 1)
+  int32_t route;            // W > 1: the final write fused with k_route's work (rt; CTAs in ticket order)
+  RouteArgs rt;
   uint32_t *err;
   uint32_t *err_host;       // with fin: see PoolArgs::fin
   uint32_t *fin;

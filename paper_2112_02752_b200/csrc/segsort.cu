@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "p2p_dev.cuh"
 
 #ifndef EMB_SEG_MATCH
 #define EMB_SEG_MATCH 1
@@ -64,14 +65,24 @@ __device__ __forceinline__ void group_bounds(const SegSortArgs &a, int g, int64_
   lo = lo < 0 ? 0 : (lo > a.nnz ? a.nnz : lo);
   hi = hi < lo ? lo : (hi > a.nnz ? a.nnz : hi);
 }
-__device__ __forceinline__ void segsort_range_body(const SegSortArgs &a) {
+// the sorted key range of one CTA: items in sorted order are keys[pa[i]] (table-local ids; `rows` =
+// invalid) with occurrence glo + ia[pa[i]], at sorted positions pos0 + i, i < n
+struct SortedRange {
+  uint32_t n = 0;
+  int64_t pos0 = 0, glo = 0;
+  const uint32_t *keys = nullptr, *pa = nullptr, *ia = nullptr;
+  uint32_t base = 0, rows = 0;
+};
+
+__device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, int work) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ uint32_t cnt[SS_WARPS][256];
   __shared__ uint32_t part[SS_THREADS / 32];
   __shared__ uint32_t wbelow[SS_WARPS], wmine[SS_WARPS];
+  SortedRange out;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int K = a.K;
-  const int g = blockIdx.x / K, bkt = blockIdx.x % K;
+  const int g = work / K, bkt = work % K;
   // CSR validation (R4; before any early return; W > 1 only -- at W = 1 the concurrent pool validates):
   // CTA (g, bkt) checks the bkt-th 1/K slice of its group's bags, so every input error is known before
   // the route publishes it. CTA (0, 0) also checks both ends and marks sorted positions no group covers
@@ -87,7 +98,7 @@ __device__ __forceinline__ void segsort_range_body(const SegSortArgs &a) {
       const int64_t o0 = a.offsets[i], o1 = a.offsets[i + 1];
       bad |= o0 < 0 || o1 < o0 || o1 > a.nnz;
     }
-    if (blockIdx.x == 0) {
+    if (work == 0) {
       const int64_t first = a.offsets[0], last = a.offsets[nb_all];
       if (tid == 0) bad |= first != 0 || last != a.nnz;
       const int64_t f = first < 0 ? 0 : (first > a.nnz ? a.nnz : first);
@@ -100,7 +111,7 @@ __device__ __forceinline__ void segsort_range_body(const SegSortArgs &a) {
   int64_t glo, ghi;
   group_bounds(a, g, glo, ghi);
   const uint32_t ng = (uint32_t)(ghi - glo);
-  if (ng == 0) return;
+  if (ng == 0) return out;
   const uint32_t base = (uint32_t)a.gbase[g];
   const uint32_t rows = a.grows[g];
   const uint32_t bits = a.gbits[g];
@@ -149,7 +160,7 @@ __device__ __forceinline__ void segsort_range_body(const SegSortArgs &a) {
     if (q < w) my_start += wmine[q];
     n += wmine[q];
   }
-  if (n == 0) return;
+  if (n == 0) return out;
   uint32_t *keys, *ia, *ib;
   if (n <= SEG_CHUNK_CAP) {
     keys = sm;
@@ -246,17 +257,184 @@ __device__ __forceinline__ void segsort_range_body(const SegSortArgs &a) {
     pa = pb;
     pb = t;
   }
-  // ---- 4. final positions: group offset of the range + rank
-  for (uint32_t i = tid; i < n; i += SS_THREADS) {
-    const uint32_t item = npass > 0 ? pa[i] : i;
-    const uint32_t lk = keys[item];
-    a.skey[glo + out_lo + i] = (lk >= rows) ? EMB_SENTINEL : base + lk;
-    a.spay[glo + out_lo + i] = (uint32_t)(glo + ia[item]);
+  if (npass == 0) {  // (a 0-bit group -- rows = 1 -- keeps the identity order)
+    for (uint32_t i = tid; i < n; i += SS_THREADS) pa[i] = i;
+    __syncthreads();
+  }
+  out.n = n;
+  out.pos0 = glo + out_lo;
+  out.glo = glo;
+  out.keys = keys;
+  out.pa = pa;
+  out.ia = ia;
+  out.base = base;
+  out.rows = rows;
+  return out;
+}
+
+// ---- 4. final positions: group offset of the range + rank
+__device__ __forceinline__ void segsort_write(const SegSortArgs &a, const SortedRange &r) {
+  for (uint32_t i = threadIdx.x; i < r.n; i += SS_THREADS) {
+    const uint32_t item = r.pa[i];
+    const uint32_t lk = r.keys[item];
+    a.skey[r.pos0 + i] = (lk >= r.rows) ? EMB_SENTINEL : r.base + lk;
+    a.spay[r.pos0 + i] = (uint32_t)(r.glo + r.ia[item]);
   }
 }
 
+// ---- 4' (W > 1): the final write fused with the route (route.cu k_route, same outputs): the CTAs
+// take their (group, range) in ticket order, which is sorted-position order, so each CTA's per-owner
+// head counts get their exclusive prefix by a decoupled look-back over the earlier CTAs. A range's
+// first item is always a segment head (ranges partition a table's key space).
+__device__ __forceinline__ void segsort_route(const SegSortArgs &a, const SortedRange &r, int work) {
+  const RouteArgs &ra = a.rt;
+  __shared__ uint32_t wcnt[SS_WARPS][P2P_MAXW];
+  __shared__ uint32_t s_excl[P2P_MAXW];
+  __shared__ uint32_t s_last;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int W = ra.p2p.world;
+  const int64_t cap = ra.p2p.cap;
+  if (tid < SS_WARPS * P2P_MAXW) (&wcnt[0][0])[tid] = 0;
+  __syncthreads();
+  // warp w: items [w*per, (w+1)*per) in rows of 32, per a multiple of 32
+  const uint32_t per = ((r.n + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;
+  const uint32_t i_lo = w * per, i_hi = min(r.n, i_lo + per);
+  auto info = [&](uint32_t i, uint32_t &lk, bool &valid, bool &head, uint32_t &o) {
+    lk = i < i_hi ? r.keys[r.pa[i]] : r.rows;
+    valid = i < i_hi && lk < r.rows;
+    const uint32_t prev = (i > 0 && i < i_hi) ? r.keys[r.pa[i - 1]] : 0xFFFFFFFFu;
+    head = valid && (i == 0 || lk != prev);
+    o = valid ? owner_of_g(r.base + lk, ra.ks) : 0u;
+  };
+  // pass 1: heads per owner for this warp
+  for (uint32_t r0 = i_lo; r0 < i_hi; r0 += 32) {
+    uint32_t lk, o;
+    bool valid, head;
+    info(r0 + lane, lk, valid, head, o);
+    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? o : 0x100u + lane);
+    const uint32_t hb = __ballot_sync(0xffffffffu, head);
+    if (valid && lane == __ffs(peers) - 1) wcnt[w][o] += __popc(peers & hb);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per owner (warp o): prefix over warps, aggregate, look-back over the earlier CTAs (32 per probe)
+  if (w < W) {
+    const int o = w;
+    const uint32_t c = lane < SS_WARPS ? wcnt[lane][o] : 0u;
+    const uint32_t incl = warp_incl_scan(c);
+    const uint32_t agg = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane < SS_WARPS) wcnt[lane][o] = incl - c;
+    const unsigned long long tag = (unsigned long long)ra.tag << 32;
+    constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_VAL = (1u << 30) - 1u;
+    volatile unsigned long long *st = reinterpret_cast<volatile unsigned long long *>(ra.status);
+    if (lane == 0) st[(int64_t)work * P2P_MAXW + o] = tag | (work == 0 ? LB_INC : LB_AGG) | agg;
+    uint32_t excl = 0;
+    if (work > 0) {
+      int64_t look = work - 1;
+      while (true) {
+        const int64_t t = look - lane;
+        unsigned long long sv = 0;
+        if (t >= 0) {
+          do {
+            sv = st[t * P2P_MAXW + o];
+          } while ((sv >> 32) != ra.tag || ((uint32_t)sv & ~LB_VAL) == 0);
+        }
+        const bool inc = t < 0 || ((uint32_t)sv & LB_INC);
+        const uint32_t m = __ballot_sync(0xffffffffu, inc);
+        const int last = m ? __ffs(m) - 1 : 31;
+        uint32_t v = (lane <= last && t >= 0) ? ((uint32_t)sv & LB_VAL) : 0u;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        excl += v;
+        if (m) break;
+        look -= 32;
+      }
+      if (lane == 0) st[(int64_t)work * P2P_MAXW + o] = tag | LB_INC | (excl + agg);
+    }
+    if (lane == 0) {
+      s_excl[o] = excl;
+      if (agg) atomicAdd(ra.tot + o, agg);
+    }
+  }
+  __syncthreads();
+  // pass 2: sorted keys / payloads, ranks, peer stores of the heads' local ids
+  const int64_t parity_off = (int64_t)(ra.p2p.epoch & 1u) * W * cap;
+  bool bad = false;
+  for (uint32_t r0 = i_lo; r0 < i_hi; r0 += 32) {
+    const uint32_t i = r0 + lane;
+    uint32_t lk, o;
+    bool valid, head;
+    info(i, lk, valid, head, o);
+    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? o : 0x100u + lane);
+    const uint32_t same = peers & __ballot_sync(0xffffffffu, head);
+    if (i < i_hi) {
+      const int64_t p = r.pos0 + i;
+      const uint32_t occ = (uint32_t)(r.glo + r.ia[r.pa[i]]);
+      a.skey[p] = valid ? r.base + lk : EMB_SENTINEL;
+      a.spay[p] = occ;
+      uint32_t sp = EMB_SENTINEL;
+      if (valid) {
+        const uint32_t incl = __popc(same & ((2u << lane) - 1u));
+        const int64_t pos = (int64_t)s_excl[o] + wcnt[w][o] + incl - 1;
+        if (pos < 0 || pos >= cap) {
+          bad = true;
+        } else {
+          sp = (o << OUT_OWNER_SHIFT) | (uint32_t)pos;
+          ra.inv[occ] = (uint32_t)(o * cap + pos);
+          if (head)
+            ra.p2p.peer_recv_keys[o][parity_off + (int64_t)ra.p2p.rank * cap + pos] = local_of_g(r.base + lk, ra.ks);
+        }
+      }
+      ra.outidx[p] = sp;
+    }
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wcnt[w][o] += __popc(same);
+    __syncwarp();
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(ra.err, EMB_DEVERR_INTERNAL);
+  // the last CTA publishes the counts + error bits and raises KEYS (one system fence per CTA)
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(ra.blk_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  if (tid == 0) *ra.blk_done = 0;
+  if (tid < W) {
+    const int o = tid;
+    const int64_t c = atomicExch(ra.tot + o, 0u);
+    ra.scnt[o] = c;
+    uint32_t eb = ld_cg_u32(ra.err) & (EMB_DEVERR_RANGE | EMB_DEVERR_INVALID);
+    if (ra.extra_err) {
+      eb |= ra.extra_err;
+      if (o == 0) atomicOr(ra.err, ra.extra_err);
+    }
+    ra.p2p.peer_xmat[o][xmat_idx(ra.p2p.epoch, 0, ra.p2p.rank)] = c;
+    ra.p2p.peer_xmat[o][xmat_idx(ra.p2p.epoch, 1, ra.p2p.rank)] = eb;
+  }
+  __syncthreads();
+  if (tid == 0) p2p_raise(ra.p2p, P2P_KEYS);
+}
+
 __global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_constant__ SegSortArgs a) {
-  segsort_range_body(a);  // (its early returns are block-uniform)
+  int work = blockIdx.x;
+  if (a.route) {  // ticket order = sorted-position order (forward progress of the look-back)
+    __shared__ uint32_t s_work;
+    if (threadIdx.x == 0) {
+      s_work = atomicAdd(a.rt.counter, 1u);
+      if (s_work == gridDim.x - 1) *a.rt.counter = 0;
+    }
+    __syncthreads();
+    work = (int)s_work;
+  }
+  const SortedRange r = segsort_range_body(a, work);  // (block-uniform)
+  if (a.route) {
+    __syncthreads();
+    segsort_route(a, r, work);
+  } else {
+    segsort_write(a, r);
+  }
   if (a.fin) {
     __syncthreads();
     if (threadIdx.x == 0) finish_publish(a.fin + 1, a.fin + 2, 2, a.err, a.err_host);
