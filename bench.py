@@ -325,8 +325,10 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
     import torch.distributed as dist
     from paper_2112_02752_b200.harness import DeviceBatch, make_layer
 
-    # stage a pool of distinct batches in HBM (inputs resident before the timed region)
-    host_batches = [synthgen.make_batch(wl, rank=rank, step=i) for i in range(POOL_BATCHES)]
+    # stage a pool of distinct batches in HBM (inputs resident before the timed region); C4's batches
+    # are ~1.8 GB each, so fewer of them (still far above the 126 MB L2)
+    nstage = POOL_BATCHES if wl.batch * wl.num_slots * wl.dim * 8 < 500e6 else 4
+    host_batches = [synthgen.make_batch(wl, rank=rank, step=i) for i in range(nstage)]
     max_nnz = max(b.nnz for b in host_batches)
     dev_batches = [DeviceBatch(b, wl.num_slots, wl.dim, local_rank) for b in host_batches]
     layer = make_layer(wl, max_batch=wl.batch, max_ids=max_nnz, world=n, rank=rank, nccl_id=nccl_id,
@@ -335,10 +337,10 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
     use_prefetch = bool(os.environ.get("EMB_BENCH_PREFETCH"))  # experiment (measured slower)
 
     def step(i):
-        db = dev_batches[i % POOL_BATCHES]
+        db = dev_batches[i % nstage]
         layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
         if use_prefetch:  # the dedup sort of step i+1 enqueued before step i's backward (W = 1)
-            nx = dev_batches[(i + 1) % POOL_BATCHES]
+            nx = dev_batches[(i + 1) % nstage]
             layer.lookup_prefetch(nx.ids, nx.offsets, nx.batch, nx.nnz, stream)
         layer.backward_update(db.dy, wl.lr, stream)
 
@@ -354,7 +356,7 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
     barrier()
     # per-step statistics (unique counts) for the byte accounting, outside the timed region
     infos = []
-    for i in range(POOL_BATCHES):
+    for i in range(nstage):
         step(i)
         infos.append(layer.step_info())  # launches counted over lookup + backward
     barrier()
@@ -379,7 +381,7 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
                   for _ in range(profile_steps)]
         layer.profile(True)
         for i in range(profile_steps):
-            db = dev_batches[i % POOL_BATCHES]
+            db = dev_batches[i % nstage]
             fwd_ev[i][0].record(stream)
             layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
             fwd_ev[i][1].record(stream)
@@ -458,8 +460,8 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
                        "library's copy streams, double-buffered), emb_host_sync before the end event"}
     config = {"workload": describe(wl, n), "global_batch": n * B, "nnz_per_gpu": N_mean,
               "unique_local": U_l, "unique_owner": U_o,
-              "l2": f"inputs larger than L2: {POOL_BATCHES} distinct staged batches cycled "
-                    f"({POOL_BATCHES} x {(hb_bytes(host_batches[0], wl)) / 1e6:.0f} MB) + "
+              "l2": f"inputs larger than L2: {nstage} distinct staged batches cycled "
+                    f"({nstage} x {(hb_bytes(host_batches[0], wl)) / 1e6:.0f} MB) + "
                     f"{layer.rows_local * 4 * (wl.dim + layer.accum_width * (wl.opt != 'sgd')) / 1e9:.1f} GB table "
                     "state per GPU"}
     out = {"value": samples_s, "ms_per_step": ms_step, "config": config, "lookups_per_s": lookups_s,

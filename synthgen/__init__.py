@@ -80,6 +80,8 @@ WORKLOADS = {
     "C3": Workload("C3", 3, _c3_rows(), 64, tuple(range(26)), 16384, "fixed", 1, "zipf", 1.05),
     # BJ:10 "large table 1B rows x dim 128 fp32 sharded over 8xB200, batch 64k, Zipf(1.2), Adagrad" (R19: 26 slots -> 1 table)
     "C4": Workload("C4", 4, (1_000_000_000,), 128, (0,) * 26, 65536, "fixed", 1, "zipf", 1.2, world=8),
+    # C4-half (BJ:10 at the 4 GPUs gpurun offers): the same structure on 5e8 rows
+    "C4h": Workload("C4h", 4, (500_000_000,), 128, (0,) * 26, 65536, "fixed", 1, "zipf", 1.2, world=4),
     # BJ:11 "hot-id stress: 26 slots, bag 64, 90% of ids from top-1k rows, 8 GPUs" (R20)
     "C5": Workload("C5", 5, _c3_rows(), 64, tuple(range(26)), 16384, "fixed", 64, "hot1k", world=8),
 }
