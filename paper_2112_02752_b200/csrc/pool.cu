@@ -145,6 +145,50 @@ __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, in
   while (cb < nbt) flush();
 }
 
+// general tile, lane-group form (D = 16, 32, 64, 128, 256): a group of LPR = D / GC lanes holds one
+// row (GC floats each: 128-bit loads) and owns whole bags, G = 32 / LPR of the tile's bags at a time;
+// per bag it walks the ids in chunks of RCH (one id per lane, RCH row loads in flight per lane) and
+// accumulates in fp64 in occurrence order (R11, same order as pool_tile_general). No per-occurrence
+// bag search: the bag's slot, output row and bounds come from the tile header through shared memory.
+template <int LPR, int GC, bool REMOTE>
+__device__ __noinline__ void pool_tile_groups(const PoolArgs &a, const int64_t *s_off, const int64_t *s_end,
+                                              const uint32_t *s_orow, const uint32_t *s_slot, int nbt) {
+  constexpr int G = 32 / LPR;
+  constexpr int RCH = LPR < 16 ? LPR : 16;  // ids per chunk (= rows in flight per lane)
+  constexpr int D = LPR * GC;
+  const int lane = threadIdx.x & 31, grp = lane / LPR, gl = lane % LPR;
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << (LPR & 31)) - 1u) << (grp * LPR));
+  for (int bi = grp; bi < nbt; bi += G) {
+    const int64_t off = s_off[bi], end = s_end[bi];
+    const uint32_t orow = s_orow[bi], slot = s_slot[bi];
+    double acc[GC];
+#pragma unroll
+    for (int c = 0; c < GC; ++c) acc[c] = 0.0;
+    for (int64_t c0 = off; c0 < end; c0 += RCH) {
+      const int64_t j = c0 + gl;
+      const uint32_t row = (gl < RCH && j < end) ? pool_row_of<REMOTE>(a, j, slot, orow) : EMB_SENTINEL;
+      VecF<GC> v[RCH];
+#pragma unroll
+      for (int r = 0; r < RCH; ++r) {  // unconditional loads (see k_pool), zeroed below
+        const uint32_t ri = __shfl_sync(gmask, row, r, LPR);
+        v[r].load_nc(pool_row_ptr<REMOTE>(a, ri, ri != EMB_SENTINEL, D, gl * GC));
+      }
+#pragma unroll
+      for (int r = 0; r < RCH; ++r) {
+        const uint32_t ri = __shfl_sync(gmask, row, r, LPR);
+        if (ri == EMB_SENTINEL) continue;
+#pragma unroll
+        for (int c = 0; c < GC; ++c) acc[c] += (double)v[r].v[c];
+      }
+    }
+    const int64_t len = end - off;
+    VecF<GC> o;
+#pragma unroll
+    for (int c = 0; c < GC; ++c) o.v[c] = (float)((a.mean && len > 1) ? __ddiv_rn(acc[c], (double)len) : acc[c]);
+    o.store_cs(a.out + (size_t)orow * D + gl * GC);
+  }
+}
+
 template <int CPL, int RCH, int MINB, bool REMOTE, int BPT>
 __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_constant__ PoolArgs a) {
   // RCH rows per batch of the single-id path (RCH * CPL floats in flight per lane)
@@ -181,6 +225,24 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
     const uint32_t orow = (bag - s * B) * S + s;
     if (a.ids && a.blen && inb) a.blen[orow] = len;
     if (__any_sync(0xffffffffu, len > 1)) {
+      const int D_ = a.dim;
+      if (D_ == 16 || D_ == 32 || D_ == 64 || D_ == 128 || D_ == 256) {  // lane groups own whole bags
+        __shared__ int64_t sh_off[POOL_THREADS / 32][32], sh_end[POOL_THREADS / 32][32];
+        __shared__ uint32_t sh_orow[POOL_THREADS / 32][32], sh_slot[POOL_THREADS / 32][32];
+        const int wi = threadIdx.x >> 5;
+        sh_off[wi][lane] = off;
+        sh_end[wi][lane] = offn;
+        sh_orow[wi][lane] = orow;
+        sh_slot[wi][lane] = s;
+        __syncwarp();
+        if (D_ == 16) pool_tile_groups<4, 4, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
+        else if (D_ == 32) pool_tile_groups<8, 4, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
+        else if (D_ == 64) pool_tile_groups<16, 4, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
+        else if (D_ == 128) pool_tile_groups<32, 4, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
+        else pool_tile_groups<32, 8, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
+        __syncwarp();
+        continue;
+      }
       const int64_t lo = __shfl_sync(0xffffffffu, off, 0);
       const int64_t hi = __shfl_sync(0xffffffffu, offn, nbt - 1);
       pool_tile_general<CPL, REMOTE>(a, lo, hi, offn, orow, s, nbt);

@@ -35,19 +35,27 @@ size_t sort_workspace_words(int64_t max_n) {
   return (size_t)4 * RS_RADIX + 4 + (size_t)4 * tiles * RS_RADIX;
 }
 
-__global__ void __launch_bounds__(512) k_sort_hist(const uint32_t *__restrict__ keys, int64_t n, int npass,
-                                                   uint32_t *__restrict__ hist) {
-  __shared__ uint32_t h[4][RS_RADIX];
-  for (int i = threadIdx.x; i < 4 * RS_RADIX; i += blockDim.x) (&h[0][0])[i] = 0;
+// all passes' digit histograms in one read of the keys: warp-private shared-memory histograms (hot-id
+// workloads -- C5: 90% of the ids on 1,000 rows per table -- hammer a few bins; a block-wide histogram
+// made every block's 512 threads contend on them, a MATCH.ANY per key and pass cost 6x more), then one
+// global atomic per non-zero bin and block
+constexpr int HIST_THREADS = 256;
+__global__ void __launch_bounds__(HIST_THREADS) k_sort_hist(const uint32_t *__restrict__ keys, int64_t n, int npass,
+                                                            uint32_t *__restrict__ hist) {
+  __shared__ uint32_t h[HIST_THREADS / 32][4][256];
+  for (int i = threadIdx.x; i < (HIST_THREADS / 32) * 4 * 256; i += blockDim.x) (&h[0][0][0])[i] = 0;
   __syncthreads();
+  const int w = threadIdx.x >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t k = keys[i];
-    for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFFu], 1u);
+    for (int p = 0; p < npass; ++p) atomicAdd(&h[w][p][(k >> (8 * p)) & 0xFFu], 1u);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < npass * RS_RADIX; i += blockDim.x) {
-    const uint32_t c = (&h[0][0])[i];
+  for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < HIST_THREADS / 32; ++q) c += h[q][i >> 8][i & 255];
     if (c) atomicAdd(&hist[i], c);
   }
 }
@@ -123,15 +131,29 @@ __global__ void __launch_bounds__(RS_THREADS) k_sort_pass(const uint32_t *__rest
       *st = FLAG_INC | my_count;
     } else {
       *st = FLAG_AGG | my_count;
+      // look back LB predecessors per round trip (independent loads), consuming them in order until
+      // an inclusive prefix; a not-yet-published one is re-probed. (One dependent L2 read per
+      // predecessor made the look-back chain through every concurrently running tile: 556 us per
+      // pass at C5's 27M keys.)
+      constexpr int LB = 8;
       int64_t look = tile - 1;
-      while (true) {
-        uint32_t s;
-        do {
-          s = *(volatile uint32_t *)(status + look * RS_RADIX + tid);
-        } while ((s & ~VAL_MASK) == 0);
-        excl += s & VAL_MASK;
-        if (s & FLAG_INC) break;
-        --look;
+      bool done = false;
+      while (!done) {
+        uint32_t sv[LB];
+#pragma unroll
+        for (int q = 0; q < LB; ++q)
+          sv[q] = look - q >= 0 ? *(volatile uint32_t *)(status + (look - q) * RS_RADIX + tid) : (FLAG_INC | 0u);
+        int used = 0;
+#pragma unroll
+        for (int q = 0; q < LB; ++q) {
+          if (done || used < q) break;  // stop at the first unpublished one (used == q while consuming)
+          const uint32_t v = sv[q];
+          if ((v & ~VAL_MASK) == 0) break;
+          excl += v & VAL_MASK;
+          ++used;
+          if (v & FLAG_INC) done = true;
+        }
+        look -= used;
       }
       *st = FLAG_INC | (excl + my_count);
     }
@@ -171,9 +193,9 @@ cudaError_t radix_sort_pairs(const SortWorkspace &ws, const uint32_t *kin, const
   e = cudaMemsetAsync(ws.status, 0, sizeof(uint32_t) * (size_t)npass * ws.max_tiles * RS_RADIX, st);
   if (e != cudaSuccess) return e;
   int hblocks = (int)((n + 4095) / 4096);
-  if (hblocks > 296) hblocks = 296;
+  if (hblocks > 148 * 4) hblocks = 148 * 4;
   if (prof) prof(prof_ctx, KID_SORT_HIST, 0, st);
-  k_sort_hist<<<hblocks, 512, 0, st>>>(kin, n, npass, ws.hist);
+  k_sort_hist<<<hblocks, HIST_THREADS, 0, st>>>(kin, n, npass, ws.hist);
   if (prof) prof(prof_ctx, KID_SORT_HIST, 1, st);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   int nl = 1;
