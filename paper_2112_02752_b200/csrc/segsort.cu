@@ -58,6 +58,9 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
 #endif
 }
 
+// bits needed for values 0..x
+__device__ __forceinline__ uint32_t bits_span(uint32_t x) { return x ? 32u - __clz(x) : 0u; }
+
 __device__ __forceinline__ void group_bounds(const SegSortArgs &a, int g, int64_t &lo, int64_t &hi) {
   const int64_t B = a.batch;
   lo = a.offsets[(int64_t)a.gslot[g] * B];
@@ -149,9 +152,14 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
     mine += __popc(__ballot_sync(0xffffffffu, bb == (uint32_t)bkt));
   }
   if (bkt == 0 && __any_sync(0xffffffffu, badid) && lane == 0) atomicOr(a.err, EMB_DEVERR_RANGE);  // (R4)
+  __shared__ uint32_t s_kmin, s_kmax;  // key span of this range (the radix passes sort key - min)
   if (lane == 0) {
     wbelow[w] = below;
     wmine[w] = mine;
+  }
+  if (tid == 0) {
+    s_kmin = 0xFFFFFFFFu;
+    s_kmax = 0u;
   }
   __syncthreads();
   uint32_t out_lo = 0, my_start = 0, n = 0;
@@ -172,6 +180,7 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
     ib = a.scratch_b + glo + out_lo;
   }
   // ---- 2. compact the range's items in occurrence order: keys[] = local id, ia[] = group index
+  uint32_t kmin_l = 0xFFFFFFFFu, kmax_l = 0u;
   {
     uint32_t cur = my_start;
     for (uint32_t r0 = s_lo; r0 < s_hi; r0 += 32) {
@@ -187,8 +196,16 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
         const uint32_t d = cur + __popc(m & lanemask_lt());
         keys[d] = lk;
         ia[d] = i;
+        kmin_l = min(kmin_l, lk);
+        kmax_l = max(kmax_l, lk);
       }
       cur += __popc(m);
+    }
+    kmin_l = __reduce_min_sync(0xffffffffu, kmin_l);
+    kmax_l = __reduce_max_sync(0xffffffffu, kmax_l);
+    if (lane == 0) {
+      atomicMin(&s_kmin, kmin_l);
+      atomicMax(&s_kmax, kmax_l);
     }
   }
   __syncthreads();
@@ -196,7 +213,10 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
   const uint32_t chunk = ((n + SS_WARPS - 1) / SS_WARPS + 31) / 32 * 32;  // rows of 32 per warp
   const uint32_t c_lo = w * chunk;
   const uint32_t c_hi = min(n, c_lo + chunk);
-  const int npass = (int)((bits + 7) / 8);
+  // passes over the range's actual key span (a few thousand values per range at C1: 2 passes instead
+  // of the table's 3)
+  const uint32_t kmin = s_kmin;
+  const int npass = (int)((min(bits, bits_span(s_kmax - kmin)) + 7) / 8);
   // sort item ordinals 0..n-1 (ping-pong pa/pb); keys[] and ia[] stay in place
   uint32_t *pa = ib;
   uint32_t *pb = (n <= SEG_CHUNK_CAP) ? sm + 3 * n : a.run_k + glo + out_lo;
@@ -206,7 +226,7 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
     __syncwarp();
     for (uint32_t p = c_lo + lane; p < c_hi; p += 32) {
       const uint32_t item = pass == 0 ? p : pa[p];
-      atomicAdd(&cnt[w][(keys[item] >> shift) & 0xFFu], 1u);
+      atomicAdd(&cnt[w][((keys[item] - kmin) >> shift) & 0xFFu], 1u);
     }
     __syncthreads();
     {
@@ -236,7 +256,7 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
       const uint32_t p = r0 + lane;
       const bool valid = p < c_hi;
       const uint32_t item = valid ? (pass == 0 ? p : pa[p]) : 0u;
-      const uint32_t d = valid ? (keys[item] >> shift) & 0xFFu : 0u;
+      const uint32_t d = valid ? ((keys[item] - kmin) >> shift) & 0xFFu : 0u;
       const uint32_t peers = digit_peers(d, valid);
       const int leader = valid ? __ffs(peers) - 1 : 0;
       uint32_t basepos = 0;
