@@ -618,7 +618,9 @@ static cudaError_t launch_grad_t(const GradArgs &a, cudaStream_t st) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO, PRECISE>, wpc * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)g_sms * per_sm;
-  const int64_t max_blocks = ((a.n + 4 * T - 1) / (4 * T) + wpc - 1) / wpc;  // >= 4 tiles per warp
+  // >= 1 tile per warp: small inputs (C1: 18K positions) spread over more warps instead of walking
+  // 4+ tiles' latency chains each; large ones fill the resident grid anyway
+  const int64_t max_blocks = ((a.n + T - 1) / T + wpc - 1) / wpc;
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
   k_grad<CPL, T, NS, MEAN, MODE, DC, MINB, LO, PRECISE><<<(unsigned)blocks, wpc * 32, smem, st>>>(a);
