@@ -111,11 +111,12 @@ def kernel_bytes(name, wl, N, SB, U, W, U_l=None):
     return None
 
 
-def nvlink_bytes(wl, U_l, W):
+def nvlink_bytes(wl, U_l, W, lo_frac=1.0):
     """Bytes one GPU sends (= receives, symmetric) over NVLink per step (SURVEY §8(d) with the
-    double-float gradient, reading R11''): keys (4 B) + pulled rows (4D) + gradient hi/lo (8D) per
-    remote distinct key."""
-    return 0 if W == 1 else (W - 1) / W * U_l * (4 + 4 * wl.dim + 8 * wl.dim)
+    double-float gradient, reading R11''): per remote distinct key its 4-B key, its 4D-byte row back and
+    its 4D-byte gradient hi half, plus the 4D-byte lo half for the fraction `lo_frac` of keys the owner
+    receives from more than one rank."""
+    return 0 if W == 1 else (W - 1) / W * U_l * (4 + 8 * wl.dim + 4 * wl.dim * lo_frac)
 
 
 # ------------------------------------------------------------------------------ clocks sampler
@@ -356,9 +357,13 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
     barrier()
     # per-step statistics (unique counts) for the byte accounting, outside the timed region
     infos = []
+    lo_fracs = []
     for i in range(nstage):
         step(i)
         infos.append(layer.step_info())  # launches counted over lookup + backward
+        if n > 1 and i < 2:  # share of received keys with more than one source (they carry the lo half)
+            _, fanin = layer.last_owner_unique()
+            lo_fracs.append(float(fanin[fanin > 1].sum()) / max(1, int(fanin.sum())))
     barrier()
     layer.profile(True)  # allocates the profiler's event pool now, outside the timed region
     layer.profile(False)
@@ -420,9 +425,10 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
                for k, v in prof.items()}
     nvl = None
     if n > 1:
-        nb = nvlink_bytes(wl, U_l, n)
+        lo_frac = max_ranks(statistics.mean(lo_fracs)) if lo_fracs else 1.0
+        nb = nvlink_bytes(wl, U_l, n, lo_frac)
         ex_us = sum(kernels[k]["us_per_launch"] for k in ("gather_push", "grad_push") if k in kernels)
-        nvl = {"bytes_per_step_per_direction": int(nb), "peak_gbs": 770.0,
+        nvl = {"bytes_per_step_per_direction": int(nb), "lo_half_share": round(lo_frac, 4), "peak_gbs": 770.0,
                "peak_source": "measured peer copy per direction, B200_PROFILING.md (900 nominal)",
                "achieved_step_gbs": round(nb / (ms_step / 1e3) / 1e9, 1),
                "frac_step": round(nb / (ms_step / 1e3) / 1e9 / 770.0, 4),

@@ -124,7 +124,8 @@ struct emb_ctx {
   uint32_t route_tag = 0;
   uint32_t *recv_keys = nullptr;     // [2][W*cap] (peer-written)
   float *uniq_rows = nullptr;        // [W*cap][D] rows pushed by their owners (peer-written)
-  float *grecv = nullptr;            // [W*cap][2D] hi / lo parts, lane-interleaved (peer-written)
+  float *grecv = nullptr;            // [2][W*cap][D] hi rows, then lo rows (peer-written)
+  uint8_t *lof = nullptr;            // [W*cap] "owner o needs the lo half of my key i" (peer-written)
   uint32_t *ok0 = nullptr, *ov0 = nullptr, *ok1 = nullptr, *ov1 = nullptr;  // owner merge
   int64_t *n_merged = nullptr;       // device: keys received this step
   int64_t *xmat = nullptr;           // [2][2][P2P_MAXW] (peer-written)
@@ -246,8 +247,9 @@ int64_t local_of_global(const emb_ctx *h, uint64_t g) { return local_of_g((uint3
 int32_t accum_width(const emb_ctx *h) { return h->opt == EMB_OPT_ROWWISE_ADAGRAD ? 1 : h->D; }
 
 // world > 1: the buffers peers write into / read from, in P2PArgs order
-constexpr int NB_PEER = 5;
+constexpr int NB_PEER = 6;
 void peer_buffers(emb_ctx *h, void *out[NB_PEER]) {
+  out[5] = h->lof;
   out[0] = h->xmat;
   out[1] = h->flags;
   out[2] = h->recv_keys;
@@ -260,6 +262,7 @@ void set_peer(emb_ctx *h, int r, void *const ptr[NB_PEER]) {
   p.peer_flags[r] = static_cast<uint64_t *>(ptr[1]);
   p.peer_recv_keys[r] = static_cast<uint32_t *>(ptr[2]);
   p.peer_grecv[r] = static_cast<float *>(ptr[3]);
+  p.peer_lof[r] = static_cast<uint8_t *>(ptr[5]);
   p.peer_uniq_rows[r] = static_cast<float *>(ptr[4]);
 }
 void init_p2p_args(emb_ctx *h) {
@@ -559,6 +562,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
     bad |= dalloc(h, &h->recv_keys, 2 * WC) != cudaSuccess;
     bad |= dalloc(h, &h->uniq_rows, (size_t)WC * h->D) != cudaSuccess;
     bad |= dalloc(h, &h->grecv, (size_t)2 * WC * h->D) != cudaSuccess;  // hi and lo parts
+    bad |= dalloc(h, &h->lof, WC) != cudaSuccess;
     bad |= dalloc(h, &h->ok0, WC) != cudaSuccess;
     bad |= dalloc(h, &h->ov0, WC) != cudaSuccess;
     bad |= dalloc(h, &h->ok1, WC) != cudaSuccess;
@@ -915,6 +919,7 @@ emb_status_t lookup_phase1(emb_ctx *h, cudaStream_t st) {
   CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
   LAUNCH(h, KID_MERGE, h->side,
          launch_merge_tree(rk, cnt, W, h->cap, h->ok0, h->ov0, h->ok1, h->ov1, h->n_merged, h->side));
+  LAUNCH(h, KID_MERGE, h->side, launch_lo_flags(px, h->ok0, h->ov0, h->n_merged, (int64_t)W * h->cap, h->side));
   LAUNCH(h, KID_GATHER_PUSH, st, launch_gather_push(px, h->w, rk, cnt, h->D, h->rows_local, h->err_dev, st));
   return EMB_OK;
 }
@@ -973,7 +978,11 @@ emb_status_t backward_phase0(emb_ctx *h, const float *d_out, double lr, cudaStre
   g.sink_mode = 2;
   g.useg = h->outidx;
   g.nout = h->cap;
+  g.lof = h->lof;
+  g.lo_stride = (int64_t)h->world * h->cap * h->D;
   g.signal_kind = P2P_GRADS;
+  // the owners' "needs lo" bytes (written after their merges, long done by now)
+  LAUNCH(h, KID_WAIT, st, launch_wait(h->p2p, P2P_LOF, h->epoch, h->err_dev, st));
   if (h->batch > 0 && h->nnz > 0 && d_out)
     LAUNCH(h, KID_GRAD_PUSH, st, launch_grad(g, st));
   else
@@ -991,7 +1000,8 @@ emb_status_t backward_phase1(emb_ctx *h, double lr, cudaStream_t st) {
   o.n_dev = h->n_merged;
   o.src_mode = 1;
   o.src = h->grecv;
-  o.src_lo = h->grecv;  // rows are 2D floats: hi / lo lane-interleaved (grad.cu store_hilo)
+  o.src_lo = h->grecv + (size_t)W * h->cap * h->D;  // lo rows (read only for keys with several sources)
+  o.lo_stride = (int64_t)W * h->cap * h->D;
   o.nsrc = (int64_t)W * h->cap;
   o.blen = nullptr;
   o.sink_mode = 0;

@@ -193,30 +193,30 @@ __device__ __forceinline__ void apply_rowwise(const GradArgs &a, const OptConst 
 // holds a region of cap rows per source; this rank's key of rank ui in o's list goes to row
 // rank*cap + ui there (peer memory over NVLink, or this rank's own buffer when o == rank)
 __device__ __forceinline__ float *out_row3(const GradArgs &a, uint32_t ui, int D) {
-  // ui = owner << OUT_OWNER_SHIFT | rank in the owner's list (written by k_route)
-  return a.p2p.peer_grecv[ui >> OUT_OWNER_SHIFT] +
-         (size_t)((int64_t)a.p2p.rank * a.p2p.cap + (ui & OUT_POS_MASK)) * (2 * D);  // (hi/lo rows)
+  // ui = owner << OUT_OWNER_SHIFT | rank in the owner's list (written by the route); the hi row
+  return a.p2p.peer_grecv[ui >> OUT_OWNER_SHIFT] + (size_t)((int64_t)a.p2p.rank * a.p2p.cap + (ui & OUT_POS_MASK)) * D;
+}
+// does the owner need the lo half of this key's partial (more than one rank sent the key)? The owner
+// wrote the byte after its merge (p2p.cu k_lo_flags, LOF flag)
+__device__ __forceinline__ bool need_lo(const GradArgs &a, uint32_t ui) {
+  return a.lof[(int64_t)(ui >> OUT_OWNER_SHIFT) * a.p2p.cap + (ui & OUT_POS_MASK)] != 0;
 }
 
-// a merged per-key partial crosses the exchange as a double-float pair: hi = fp32(G), lo = fp32(G - hi)
-// (hi + lo carries ~48 bits, so partials of different ranks that cancel at the owner keep the fp64
-// result; an fp32 partial alone failed the tolerance on hot keys, reading R11'' in DESIGN.md). Rows of
-// the owner's region are 2D floats, lane-interleaved: lane l's 2*CPL floats (its CPL hi values, then
-// its CPL lo values) sit at 2*l*CPL, so each lane stores (and the owner's lane loads) one contiguous
-// 16*CPL/2-byte piece -- 128-bit peer stores.
+// a merged per-key partial crosses the exchange as a double-float pair: hi = fp32(G) into the owner's
+// hi region, lo = fp32(G - hi) into its lo region (lo_stride floats further) -- only when the owner
+// receives the key from more than one rank: hi + lo carries ~48 bits, so partials of different ranks
+// that cancel keep the fp64 result (an fp32 partial alone failed the tolerance on hot keys, reading
+// R11''); a key with one source is applied from g = fp32(G) = hi anyway. ~80% of the keys at W = 2.
 template <int CPL>
-__device__ __forceinline__ void store_hilo(float *dst, const double (&g)[CPL]) {
-  float o[2 * CPL];
+__device__ __forceinline__ void store_hilo(const GradArgs &a, float *dst_hi, const double (&g)[CPL], bool lo_too) {
+  VecF<CPL> hi, lo;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
-    o[c] = (float)g[c];
-    o[CPL + c] = (float)__dsub_rn(g[c], (double)o[c]);
+    hi.v[c] = (float)g[c];
+    lo.v[c] = (float)__dsub_rn(g[c], (double)hi.v[c]);
   }
-#pragma unroll
-  for (int c = 0; c < 2 * CPL; c += 4)
-    asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + c), "f"(o[c]), "f"(o[c + 1]), "f"(o[c + 2]),
-                 "f"(o[c + 3])
-                 : "memory");
+  stg_frag<CPL>(dst_hi, hi);
+  if (lo_too) stg_frag<CPL>(dst_hi + a.lo_stride, lo);
 }
 
 // the last CTA of the grid to finish raises the exchange flag: one system-scope fence per CTA, by the
@@ -317,7 +317,8 @@ __device__ __noinline__ void span_piece(const GradArgs &a, const DAcc<CPL> acc, 
     }
   }
   if constexpr (MODE == 3) {
-    store_hilo<CPL>(out_row3(a, a.useg[pos], D) + 2 * col, tot);
+    const uint32_t ui = a.useg[pos];
+    store_hilo<CPL>(a, out_row3(a, ui, D) + col, tot, need_lo(a, ui));
   } else if constexpr (MODE == 4) {
     const uint32_t lrow = key & a.lmask;
     const size_t off = (size_t)lrow * D + col;
@@ -340,6 +341,7 @@ struct TileMeta {
   uint32_t key;   // sorted key (EMB_SENTINEL = invalid / beyond the range)
   int32_t len;    // bag length (mean pooling)
   uint32_t uo;    // MODE 3: rank of the key in its owner's list
+  uint32_t lo;    // MODE 3: the owner needs the lo half (k_lo_flags)
   uint32_t vmask, hmask, tmask;  // warp-uniform: valid / head / tail
 };
 
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
     const int64_t t0 = p_lo + j * T;
     const int cnt = (int)((p_hi - t0) < T ? (p_hi - t0) : T);
     int32_t len = 1;
-    uint32_t uo = 0;
+    uint32_t uo = 0, lo_flag = 0;
     if (k != EMB_SENTINEL) {
       if ((int64_t)srow >= a.nsrc) bad = true;
       else if (MEAN) len = a.blen[srow];
@@ -413,6 +415,7 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
       if (!SINK_OPT) {
         uo = uo_in;
         if ((int64_t)(uo & OUT_POS_MASK) >= a.nout || (uo >> OUT_OWNER_SHIFT) >= (uint32_t)a.p2p.world) bad = true;
+        else lo_flag = need_lo(a, uo);  // (consumed NS tiles later: the load is off the critical path)
       }
     }
     uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
@@ -433,16 +436,19 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
     m.key = k;
     m.len = len;
     m.uo = uo;
+    m.lo = lo_flag;
     // async copies: chunk q = it*32 + lane of the tile's rows, row i = q / C16, 16-B chunk c = q % C16
-    // (a LO contribution row -- hi/lo interleaved -- is 2D floats)
+    // (LO: the hi row, and the lo row only where the segment has more than one contribution)
     const uint32_t sb = wbase + (uint32_t)(s * stage_floats * 4);
-    constexpr int RW = LO ? 2 : 1;  // contribution row width in units of D
-    for (int q0 = 0; q0 < T * C16 * RW; q0 += 32) {
+    const uint32_t lomask = m.vmask & ~(m.hmask & m.tmask);
+    for (int q0 = 0; q0 < T * C16; q0 += 32) {
       const int q = q0 + lane;
-      const int i = q / (C16 * RW), c = q - i * (C16 * RW);
+      const int i = q / C16, c = q - i * C16;
       const uint32_t ri = __shfl_sync(0xffffffffu, srow, i < T ? i : 0);
-      if (i < T && ((m.vmask >> i) & 1u))
-        cp_async16(sb + (uint32_t)((i * RW * D + c * 4) * 4), src_base + (size_t)ri * (RW * D) + c * 4);
+      const uint32_t off = (uint32_t)((i * D + c * 4) * 4);
+      if (i < T && ((m.vmask >> i) & 1u)) cp_async16(sb + off, src_base + (size_t)ri * D + c * 4);
+      if (LO && i < T && ((lomask >> i) & 1u))
+        cp_async16(sb + (uint32_t)(T * D * 4) + off, src_base + a.lo_stride + (size_t)ri * D + c * 4);
     }
     if (SINK_OPT) {
       const unsigned long long wrow = (unsigned long long)(k & a.lmask) * D;
@@ -511,13 +517,19 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
         for (int c = 0; c < CPL; ++c) acc.v[c] = hd ? 0.0 : acc.v[c];
         begins = begins || hd;
         VecF<CPL> v;
-        if constexpr (LO) {  // a received per-key partial = hi + lo (double-float, R11''), lane-interleaved
-          VecF<2 * CPL> hl;
-          if (active) lds_frag<2 * CPL>(hl, sbase + 4u * (uint32_t)(2 * i * D + col));  // (sbase has +4*col)
-          else hl.zero();
+        if constexpr (LO) {  // a received per-key partial = hi (+ lo where the key has several sources)
+          if (active) lds_frag<CPL>(v, sbase + 4u * (uint32_t)(i * D));
+          else v.zero();
+          if (!((hmask >> i) & (tmask >> i) & 1u)) {
+            VecF<CPL> vl;
+            if (active) lds_frag<CPL>(vl, sbase + 4u * (uint32_t)((T + i) * D));
+            else vl.zero();
 #pragma unroll
-          for (int c = 0; c < CPL; ++c)
-            acc.v[c] = __dadd_rn(__dadd_rn(acc.v[c], (double)hl.v[c]), (double)hl.v[CPL + c]);
+            for (int c = 0; c < CPL; ++c) acc.v[c] = __dadd_rn(__dadd_rn(acc.v[c], (double)v.v[c]), (double)vl.v[c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) acc.v[c] = __dadd_rn(acc.v[c], (double)v.v[c]);
+          }
         } else if constexpr (MEAN) {
           if (active) lds_frag<CPL>(v, sbase + 4u * (uint32_t)(i * D));
           else v.zero();
@@ -537,7 +549,8 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
           if (begins) {  // complete inside the range
             if constexpr (!SINK_OPT) {
               const uint32_t ui = __shfl_sync(0xffffffffu, m.uo, i);
-              if (active) store_hilo<CPL>(out_row3(a, ui, D) + 2 * col, acc.v);
+              const bool lo_i = __shfl_sync(0xffffffffu, m.lo, i);
+              if (active) store_hilo<CPL>(a, out_row3(a, ui, D) + col, acc.v, lo_i);
             } else if constexpr (MODE == 4) {
               VecF<CPL> wv;
               if (active) lds_frag<CPL>(wv, sbase + 4u * (uint32_t)((OFF_W + i) * D));

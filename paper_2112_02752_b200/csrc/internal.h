@@ -52,7 +52,7 @@ enum KernelId {
 // sources' runs end. Flags are per-(kind, source) epoch words raised in every peer; a wait requires
 // EXACTLY the expected epoch (a rank that fell behind times out instead of reading stale buffers).
 constexpr int P2P_MAXW = 16;  // == EMB_MAX_WORLD
-enum { P2P_KEYS = 0, P2P_ROWS = 1, P2P_GRADS = 2, P2P_NKIND = 3 };
+enum { P2P_KEYS = 0, P2P_ROWS = 1, P2P_GRADS = 2, P2P_LOF = 3, P2P_NKIND = 4 };
 // xmat layout (int64): [parity][0][s] = keys received from source s, [parity][1][s] = input-error
 // bits of source s in this step (parity = epoch & 1: double-buffered, a fast peer may already write
 // step e+1 while this rank still reads step e)
@@ -69,8 +69,10 @@ struct P2PArgs {
   uint64_t *peer_flags[P2P_MAXW];
   int64_t *peer_xmat[P2P_MAXW];
   uint32_t *peer_recv_keys[P2P_MAXW];   // [2][W * cap] owner-local ids, region s = source s
-  float *peer_grecv[P2P_MAXW];          // [W * cap][2D] merged per-key gradients as double-float
-                                        // (hi / lo lane-interleaved), region s = source s
+  float *peer_grecv[P2P_MAXW];          // [2][W * cap][D] merged per-key gradients as double-float:
+                                        // hi rows, then lo rows; region s = source s
+  uint8_t *peer_lof[P2P_MAXW];          // [W * cap] requester side: does owner o need the lo half of
+                                        // my key of rank i (region o, written by owner o)
   float *peer_uniq_rows[P2P_MAXW];      // [W * cap][D] rows received by the requester, region o = owner o
 };
 // wait (one thread, bounded) until every source raised `kind` with exactly `epoch`
@@ -85,6 +87,10 @@ cudaError_t launch_signal(const P2PArgs &a, int kind, uint32_t err_bits, cudaStr
 // profiles/r02_ipc_gather_bench.log, so rows are pushed by the owner, not pulled by the requester.)
 cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t *recv_keys, const int64_t *counts,
                                int dim, int64_t rows_local, uint32_t *err, cudaStream_t st);
+// owner, after its merge: for every received key, whether another rank sent the same key (its merged
+// neighbours): that byte into the requester's lof region for this owner; the last block raises LOF
+cudaError_t launch_lo_flags(const P2PArgs &a, const uint32_t *okey, const uint32_t *opay, const int64_t *n_merged,
+                            int64_t max_n, cudaStream_t st);
 
 // A3+A4 fused (route.cu): over the sorted fused keys, per distinct key (segment head) its owner o and
 // its rank `sendpos` among this rank's distinct keys owned by o (ascending g); the head's local id is
@@ -196,8 +202,10 @@ struct GradArgs {
   const int32_t *blen;     // [B*S] bag length by dY row (mean) or nullptr
   int32_t batch, num_slots;
   const float *src;        // mode 1
-  const float *src_lo;     // non-null (W > 1 owner side): src rows are 2D-float double-float partials
-                           // (hi / lo lane-interleaved, grad.cu store_hilo)
+  const float *src_lo;     // non-null (W > 1 owner side): src rows are double-float partials, the lo
+                           // rows lo_stride floats after the hi rows (grad.cu store_hilo)
+  int64_t lo_stride;       // floats from a hi row to its lo row (W * cap * D)
+  const uint8_t *lof;      // sink 2: per (owner, rank) "the owner needs the lo half" bytes
   // sink: 0 = optimizer apply on table rows (row = key & lmask); 2 = the merged fp32 row stored
   // straight into the owner's gradient region through peer memory (requester side at W > 1)
   int32_t sink_mode;

@@ -1,10 +1,12 @@
 """World-size-2 and -8 CPU tests (gloo) of the N>1 host logic (-m "not gpu"):
   * the ncclUniqueId broadcast and the max-over-ranks timing reduction of paper_2112_02752_b200.dist;
-  * the row-sharded exchange protocol that libemb implements with its peer-memory kernels (or NCCL,
-    DESIGN.md §8), replayed with torch.distributed all-to-alls and oracle arithmetic per rank: per-rank dedup -> owner-major send
-    lists + counts (X0) -> keys to owners (X1) -> rows back (X2) -> pool -> per-unique-key gradients
-    to owners (X3) -> source-rank-order merge -> update. Its result must equal the single-process
-    oracle on the same per-rank batches (SPEC idea "distributed == serial").
+  * the row-sharded exchange protocol that libemb implements with its peer-memory kernels (DESIGN.md
+    §8), replayed with torch.distributed all-to-alls and oracle arithmetic per rank: per-rank dedup ->
+    per-owner ascending key lists + counts (libemb: the route, KEYS) -> keys to owners -> the owners'
+    rows back (libemb: gather-push, ROWS) -> pool -> per-unique-key gradients to owners (libemb: the
+    requester merge, GRADS) -> source-rank-order merge -> update. Its result must equal the
+    single-process oracle on the same per-rank batches (SPEC idea "distributed ==
+    serial").
 """
 import os
 import socket
