@@ -409,8 +409,10 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
     hbm = step_bytes(wl, N_mean, SB, U_l, U_o, n)
     launches_per_step = statistics.mean(inf["launches"] for inf in infos)
 
-    # dominant kernel = largest summed device time
-    dom, (dom_ms, dom_cnt) = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 0))
+    # dominant kernel = largest summed device time among the step kernels with a byte model (the owner
+    # merge / flag kernels run on a side stream, hidden behind the gather-push and the pool)
+    modeled = {k: v for k, v in prof.items() if kernel_bytes(k, wl, 1, 1, 1, n, 1) is not None}
+    dom, (dom_ms, dom_cnt) = max(modeled.items(), key=lambda kv: kv[1][0]) if modeled else ("none", (0.0, 0))
     kb = kernel_bytes(dom, wl, N_mean, SB, U_o, n, U_l)
     roof = None
     if kb is not None and dom_cnt:

@@ -47,7 +47,7 @@ std::string g_create_error = "no error";
 
 const char *kKernelNames[KID_COUNT] = {"keys",      "sort_hist", "sort_pass", "pool",        "grad_apply",
                                        "unique",    "route",     "gather_push", "grad_push",   "signal",
-                                       "init",      "owner_merge", "p2p_wait"};
+                                       "init",      "owner_merge", "p2p_wait",  "lo_flags"};
 
 uint32_t bits_for(uint64_t x) {  // smallest b with x < 2^b (x >= 0)
   uint32_t b = 0;
@@ -919,7 +919,7 @@ emb_status_t lookup_phase1(emb_ctx *h, cudaStream_t st) {
   CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
   LAUNCH(h, KID_MERGE, h->side,
          launch_merge_tree(rk, cnt, W, h->cap, h->ok0, h->ov0, h->ok1, h->ov1, h->n_merged, h->side));
-  LAUNCH(h, KID_MERGE, h->side, launch_lo_flags(px, h->ok0, h->ov0, h->n_merged, (int64_t)W * h->cap, h->side));
+  LAUNCH(h, KID_LOFLAGS, h->side, launch_lo_flags(px, h->ok0, h->ov0, h->n_merged, (int64_t)W * h->cap, h->side));
   LAUNCH(h, KID_GATHER_PUSH, st, launch_gather_push(px, h->w, rk, cnt, h->D, h->rows_local, h->err_dev, st));
   return EMB_OK;
 }

@@ -509,8 +509,21 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
       }
       const uint32_t sbase = wbase + (uint32_t)(s * stage_floats * 4) + 4u * (uint32_t)col;
       const uint32_t vmask = m.vmask, hmask = m.hmask, tmask = m.tmask;
+      // a full tile inside one segment (no head, no tail: long hot-key segments, C5) only accumulates
+      // -- without the per-position mask bookkeeping of the general walk below
+      const bool plain = !MEAN && !LO && (hmask | tmask) == 0 && vmask == ((1u << T) - 1u);
+      if (plain) {
 #pragma unroll
-      for (int i = 0; i < T; ++i) {  // compile-time positions: constant shared offsets
+        for (int i = 0; i < T; ++i) {
+          VecF<CPL> v;
+          if (active) lds_frag<CPL>(v, sbase + 4u * (uint32_t)(i * D));
+          else v.zero();
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc.v[c] = __dadd_rn(acc.v[c], (double)v.v[c]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < T && !plain; ++i) {  // compile-time positions: constant shared offsets
         if (!((vmask >> i) & 1u)) continue;
         const bool hd = (hmask >> i) & 1u;
 #pragma unroll

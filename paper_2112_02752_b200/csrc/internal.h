@@ -43,6 +43,7 @@ enum KernelId {
   KID_INIT,
   KID_MERGE,
   KID_WAIT,
+  KID_LOFLAGS,
   KID_COUNT
 };
 
