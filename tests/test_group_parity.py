@@ -84,7 +84,10 @@ def _run_group(torch, case, world, shard="cyclic", devices=None):
     ("c3", 2, "cyclic"), ("c3", 4, "cyclic"), ("c3", 2, "block"), ("c3", 3, "block"),
     ("hot", 2, "cyclic"), ("hot", 4, "block"), ("c3rw", 2, "cyclic"), ("c3rw", 4, "cyclic"),
     ("gen", 2, "cyclic"), ("gen", 4, "cyclic"), ("edge", 2, "cyclic"), ("edge", 4, "block"),
-    ("c5", 2, "cyclic"), ("c3full", 2, "cyclic"), ("c3full", 4, "cyclic")])
+    ("c5", 2, "cyclic"), ("c3full", 2, "cyclic"), ("c3full", 4, "cyclic"),
+    # W = 8 (BJ:9-11's GPU count) and 16 (EMB_MAX_WORLD) emulated on one GPU: 3- and 4-pass merge
+    # trees, 8- / 16-way regions and flags
+    ("c3", 8, "cyclic"), ("hot", 8, "block"), ("gen", 8, "cyclic"), ("c3rw", 8, "cyclic"), ("c3", 16, "cyclic")])
 def test_group_row_sharded_parity(torch, case, world, shard):
     _run_group(torch, case, world, shard)
 
