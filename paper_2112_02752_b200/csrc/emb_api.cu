@@ -919,7 +919,11 @@ emb_status_t lookup_phase1(emb_ctx *h, cudaStream_t st) {
   CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
   LAUNCH(h, KID_MERGE, h->side,
          launch_merge_tree(rk, cnt, W, h->cap, h->ok0, h->ov0, h->ok1, h->ov1, h->n_merged, h->side));
-  LAUNCH(h, KID_LOFLAGS, h->side, launch_lo_flags(px, h->ok0, h->ov0, h->n_merged, (int64_t)W * h->cap, h->side));
+  // (no fused error publish here: the per-block barrier + atomic it adds to the 1,664 short pool blocks
+  // cost more than the separate publish kernel, W = 2 297.6 -> 304-307 us/step)
+  LAUNCH(h, KID_LOFLAGS, h->side,
+         launch_lo_flags(px, h->ok0, h->ov0, h->n_merged, (int64_t)W * h->cap, nullptr, h->err_dev, h->err_host_dev,
+                         h->side));
   LAUNCH(h, KID_GATHER_PUSH, st, launch_gather_push(px, h->w, rk, cnt, h->D, h->rows_local, h->err_dev, st));
   return EMB_OK;
 }

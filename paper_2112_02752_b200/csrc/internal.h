@@ -90,8 +90,9 @@ cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t 
                                int dim, int64_t rows_local, uint32_t *err, cudaStream_t st);
 // owner, after its merge: for every received key, whether another rank sent the same key (its merged
 // neighbours): that byte into the requester's lof region for this owner; the last block raises LOF
+// fin != nullptr: the later of this kernel and the pool publishes the error word (PoolArgs::fin)
 cudaError_t launch_lo_flags(const P2PArgs &a, const uint32_t *okey, const uint32_t *opay, const int64_t *n_merged,
-                            int64_t max_n, cudaStream_t st);
+                            int64_t max_n, uint32_t *fin, uint32_t *err, uint32_t *err_host, cudaStream_t st);
 
 // A3+A4 fused (route.cu): over the sorted fused keys, per distinct key (segment head) its owner o and
 // its rank `sendpos` among this rank's distinct keys owned by o (ascending g); the head's local id is

@@ -126,7 +126,7 @@ cudaError_t launch_gather_push(const P2PArgs &a, const float *w, const uint32_t 
 
 // owner: per merged received key, "another rank sent it too" -> the requester's lof byte
 __global__ void k_lo_flags(P2PArgs a, const uint32_t *__restrict__ okey, const uint32_t *__restrict__ opay,
-                           const int64_t *__restrict__ n_merged) {
+                           const int64_t *__restrict__ n_merged, uint32_t *fin, uint32_t *err, uint32_t *err_host) {
   const int64_t n = *n_merged;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = okey[p];
@@ -136,13 +136,14 @@ __global__ void k_lo_flags(P2PArgs a, const uint32_t *__restrict__ okey, const u
     a.peer_lof[s][(int64_t)a.rank * a.cap + i] = multi ? 1 : 0;
   }
   p2p_signal_last_block(a, P2P_LOF);
+  if (fin && threadIdx.x == 0) finish_publish(fin + 1, fin + 2, 2, err, err_host);  // (the later of this and the pool)
 }
 cudaError_t launch_lo_flags(const P2PArgs &a, const uint32_t *okey, const uint32_t *opay, const int64_t *n_merged,
-                            int64_t max_n, cudaStream_t st) {
+                            int64_t max_n, uint32_t *fin, uint32_t *err, uint32_t *err_host, cudaStream_t st) {
   int64_t blocks = (max_n + 255) / 256;
   if (blocks > 148 * 4) blocks = 148 * 4;
   if (blocks < 1) blocks = 1;
-  k_lo_flags<<<(unsigned)blocks, 256, 0, st>>>(a, okey, opay, n_merged);
+  k_lo_flags<<<(unsigned)blocks, 256, 0, st>>>(a, okey, opay, n_merged, fin, err, err_host);
   return cudaGetLastError();
 }
 

@@ -151,16 +151,21 @@ __device__ __noinline__ void pool_tile_general(const PoolArgs &a, int64_t lo, in
 // accumulates in fp64 in occurrence order (R11, same order as pool_tile_general). No per-occurrence
 // bag search: the bag's slot, output row and bounds come from the tile header through shared memory.
 template <int LPR, int GC, bool REMOTE>
-__device__ __noinline__ void pool_tile_groups(const PoolArgs &a, const int64_t *s_off, const int64_t *s_end,
-                                              const uint32_t *s_orow, const uint32_t *s_slot, int nbt) {
+__device__ __noinline__ void pool_tile_groups(const PoolArgs &a, int64_t my_off, int64_t my_end, uint32_t my_orow,
+                                              uint32_t my_slot, int nbt) {
   constexpr int G = 32 / LPR;
   constexpr int RCH = LPR < 16 ? LPR : 16;  // ids per chunk (= rows in flight per lane)
   constexpr int D = LPR * GC;
   const int lane = threadIdx.x & 31, grp = lane / LPR, gl = lane % LPR;
   const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << (LPR & 31)) - 1u) << (grp * LPR));
-  for (int bi = grp; bi < nbt; bi += G) {
-    const int64_t off = s_off[bi], end = s_end[bi];
-    const uint32_t orow = s_orow[bi], slot = s_slot[bi];
+  // (the tile header -- lane l holds bag l's bounds -- is read with warp-uniform shuffles: shared
+  // memory for it kept a pool block from sharing an SM with a sort CTA)
+  for (int it = 0; it * G < nbt; ++it) {
+    const int bi = it * G + grp;
+    const int src = bi < 32 ? bi : 31;
+    const int64_t off = __shfl_sync(0xffffffffu, my_off, src), end = __shfl_sync(0xffffffffu, my_end, src);
+    const uint32_t orow = __shfl_sync(0xffffffffu, my_orow, src), slot = __shfl_sync(0xffffffffu, my_slot, src);
+    if (bi >= nbt) continue;
     double acc[GC];
 #pragma unroll
     for (int c = 0; c < GC; ++c) acc[c] = 0.0;
@@ -227,20 +232,11 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
     if (__any_sync(0xffffffffu, len > 1)) {
       const int D_ = a.dim;
       if (D_ == 16 || D_ == 32 || D_ == 64 || D_ == 128 || D_ == 256) {  // lane groups own whole bags
-        __shared__ int64_t sh_off[POOL_THREADS / 32][32], sh_end[POOL_THREADS / 32][32];
-        __shared__ uint32_t sh_orow[POOL_THREADS / 32][32], sh_slot[POOL_THREADS / 32][32];
-        const int wi = threadIdx.x >> 5;
-        sh_off[wi][lane] = off;
-        sh_end[wi][lane] = offn;
-        sh_orow[wi][lane] = orow;
-        sh_slot[wi][lane] = s;
-        __syncwarp();
-        if (D_ == 16) pool_tile_groups<4, 4, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
-        else if (D_ == 32) pool_tile_groups<8, 4, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
-        else if (D_ == 64) pool_tile_groups<16, 4, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
-        else if (D_ == 128) pool_tile_groups<32, 4, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
-        else pool_tile_groups<32, 8, REMOTE>(a, sh_off[wi], sh_end[wi], sh_orow[wi], sh_slot[wi], nbt);
-        __syncwarp();
+        if (D_ == 16) pool_tile_groups<4, 4, REMOTE>(a, off, offn, orow, s, nbt);
+        else if (D_ == 32) pool_tile_groups<8, 4, REMOTE>(a, off, offn, orow, s, nbt);
+        else if (D_ == 64) pool_tile_groups<16, 4, REMOTE>(a, off, offn, orow, s, nbt);
+        else if (D_ == 128) pool_tile_groups<32, 4, REMOTE>(a, off, offn, orow, s, nbt);
+        else pool_tile_groups<32, 8, REMOTE>(a, off, offn, orow, s, nbt);
         continue;
       }
       const int64_t lo = __shfl_sync(0xffffffffu, off, 0);
