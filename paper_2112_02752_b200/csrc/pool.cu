@@ -246,6 +246,30 @@ __global__ void __launch_bounds__(POOL_THREADS, MINB) k_pool(const __grid_consta
     }
     // single-id bags: copy the row (exact)
     const uint32_t row = (len == 1) ? pool_row_of<REMOTE>(a, off, s, orow) : EMB_SENTINEL;
+    if (CPL == 2 && D == 64) {
+      // D = 64: a half-warp per row (16 lanes x float4: 128-bit loads and stores), the two halves on
+      // alternate bags -- half the load / store / shuffle instructions of the 32-lane float2 rows for
+      // the same bytes in flight per warp (the north_star's 128-bit row loads)
+      const int half = lane >> 4, hl = lane & 15;
+#pragma unroll
+      for (int c0 = 0; c0 < 32; c0 += 32) {
+        float4 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {  // unconditional loads (see below)
+          const uint32_t ri = __shfl_sync(0xffffffffu, row, c0 + 2 * r + half);
+          v[r] = ld_nc_f4(reinterpret_cast<const float4 *>(pool_row_ptr<REMOTE>(a, ri, ri != EMB_SENTINEL, 64, hl * 4)));
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int b = c0 + 2 * r + half;
+          const uint32_t ri = __shfl_sync(0xffffffffu, row, b);
+          const uint32_t oi = __shfl_sync(0xffffffffu, orow, b);
+          if (ri == EMB_SENTINEL) v[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (b < nbt) st_cs_f4(reinterpret_cast<float4 *>(a.out + (size_t)oi * 64 + hl * 4), v[r]);
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int c0 = 0; c0 < 32; c0 += RCH) {
       if (c0 >= nbt) break;
