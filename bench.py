@@ -335,12 +335,17 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
     layer = make_layer(wl, max_batch=wl.batch, max_ids=max_nnz, world=n, rank=rank, nccl_id=nccl_id,
                        device=local_rank)
     stream = torch.cuda.current_stream()
-    use_prefetch = bool(os.environ.get("EMB_BENCH_PREFETCH"))  # experiment (measured slower)
+    # emb_lookup_prefetch: the next step's first phase (W = 1: the dedup sort; W > 1: sort + route)
+    # enqueued before this step's backward, so it overlaps the gradient passes (a training loop knows
+    # its next batch). Default on; EMB_BENCH_PREFETCH=0 turns it off. Within each loop the first step
+    # runs its own first phase and the last prefetches nothing, so every step's work is inside the
+    # loop that times it.
+    use_prefetch = os.environ.get("EMB_BENCH_PREFETCH", "1") == "1"
 
-    def step(i):
+    def step(i, last=False):
         db = dev_batches[i % nstage]
         layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
-        if use_prefetch:  # the dedup sort of step i+1 enqueued before step i's backward (W = 1)
+        if use_prefetch and not last:
             nx = dev_batches[(i + 1) % nstage]
             layer.lookup_prefetch(nx.ids, nx.offsets, nx.batch, nx.nnz, stream)
         layer.backward_update(db.dy, wl.lr, stream)
@@ -353,13 +358,13 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
         return float(t.item())
 
     for i in range(args.warmup):
-        step(i)
+        step(i, i == args.warmup - 1)
     barrier()
     # per-step statistics (unique counts) for the byte accounting, outside the timed region
     infos = []
     lo_fracs = []
     for i in range(nstage):
-        step(i)
+        step(i, i == nstage - 1)
         infos.append(layer.step_info())  # launches counted over lookup + backward
         if n > 1 and i < 2:  # share of received keys with more than one source (they carry the lo half)
             _, fanin = layer.last_owner_unique()
@@ -373,7 +378,7 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for i in range(args.steps):
-            step(i)
+            step(i, i == args.steps - 1)
         ev1.record(stream)
         torch.cuda.synchronize()
     t_ms = max_ranks(ev0.elapsed_time(ev1))
@@ -385,6 +390,8 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
         fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in range(profile_steps)]
         layer.profile(True)
+        # no prefetch here: fwd_ms is the whole lookup (sort included) and every kernel's time is its
+        # own, not stretched by a concurrent prefetched sort
         for i in range(profile_steps):
             db = dev_batches[i % nstage]
             fwd_ev[i][0].record(stream)
@@ -471,7 +478,9 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
               "l2": f"inputs larger than L2: {nstage} distinct staged batches cycled "
                     f"({nstage} x {(hb_bytes(host_batches[0], wl)) / 1e6:.0f} MB) + "
                     f"{layer.rows_local * 4 * (wl.dim + layer.accum_width * (wl.opt != 'sgd')) / 1e9:.1f} GB table "
-                    "state per GPU"}
+                    "state per GPU",
+              "prefetch": ("emb_lookup_prefetch: the next step's sort + route (W = 1: sort) overlaps each backward "
+                           "inside the timed loop" if use_prefetch else "off")}
     out = {"value": samples_s, "ms_per_step": ms_step, "config": config, "lookups_per_s": lookups_s,
            "fwd_ms": fwd_ms,
            "step_roofline": {"bound": "hbm", "algorithmic_bytes": int(hbm),

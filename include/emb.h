@@ -144,13 +144,20 @@ emb_status_t emb_get_unique_id(void *out128);
 emb_status_t emb_lookup(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                         int64_t nnz, float *out, void *cuda_stream);
 
-/* Optional pipelining (world == 1 with a monotone slot -> table map; a no-op returning EMB_OK
- * otherwise): start the per-table dedup sort of the NEXT emb_lookup's inputs on the library's internal
- * stream, ordered after the work already enqueued on cuda_stream (so the inputs must be ready there)
- * but not after work enqueued later. Called between emb_lookup(k) and emb_backward_update(k), the
- * sort of step k+1 overlaps the gradient pass of step k. The next emb_lookup consumes it when it is
- * called with the same ids / offsets pointers and batch / nnz (any other call discards it); ids and
- * offsets must stay valid and unmodified until then. Results are identical with or without it. */
+/* Optional pipelining (per-table sort path, i.e. a monotone slot -> table map; a no-op returning
+ * EMB_OK otherwise or for an empty batch): start the first part of the NEXT emb_lookup on the library's
+ * internal stream, ordered after the work already enqueued on cuda_stream (so the inputs must be ready
+ * there) but not after work enqueued later. Called between emb_lookup(k) and emb_backward_update(k),
+ * it overlaps the gradient pass of step k. Results are identical with or without it.
+ *  - world == 1: the per-table dedup sort. The next emb_lookup consumes it when called with the same
+ *    ids / offsets pointers and batch / nnz; any other call discards it.
+ *  - world > 1: the dedup sort AND the route: the step's distinct keys are stored into their owners'
+ *    receive regions (the prefetch is the first phase of the next collective step, so it cannot be
+ *    withdrawn). The next emb_lookup must pass the same ids / offsets pointers and batch / nnz; if it
+ *    does not, it returns EMB_ERR_INVALID after taking part with an empty batch and the step updates
+ *    nothing on any rank. A second prefetch before that lookup returns EMB_ERR_STATE. Ranks may mix
+ *    prefetching and plain lookups freely. Group handles use emb_lookup_prefetch_group.
+ * ids and offsets must stay valid and unmodified until the consuming emb_lookup. */
 emb_status_t emb_lookup_prefetch(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                                  int64_t nnz, void *cuda_stream);
 
@@ -169,6 +176,12 @@ emb_status_t emb_backward_update(emb_handle_t h, const float *d_out, double lr, 
 emb_status_t emb_lookup_group(emb_handle_t *hs, int32_t n, const int64_t *const *ids, const int64_t *const *offsets,
                               const int32_t *batch, const int64_t *nnz, float *const *out, void *const *streams);
 emb_status_t emb_backward_update_group(emb_handle_t *hs, int32_t n, const float *const *d_out, double lr,
+                                       void *const *streams);
+/* Group form of emb_lookup_prefetch: per rank r, emb_lookup_prefetch(hs[r], ids[r], offsets[r],
+ * batch[r], nnz[r], streams[r]) (streams may be NULL: default streams). The next emb_lookup_group
+ * consumes the prefetched first phases. Returns the first rank's error, if any. */
+emb_status_t emb_lookup_prefetch_group(emb_handle_t *hs, int32_t n, const int64_t *const *ids,
+                                       const int64_t *const *offsets, const int32_t *batch, const int64_t *nnz,
                                        void *const *streams);
 
 /* End-to-end variants over HOST buffers (pinned memory, else the copies serialise): ASYNCHRONOUS --

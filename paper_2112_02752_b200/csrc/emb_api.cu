@@ -93,7 +93,10 @@ struct emb_ctx {
     int32_t batch = 0;
     int64_t nnz = 0;
     int set = 0;
+    uint64_t epoch = 0;  // W > 1: the step whose first phase (sort + route) the prefetch ran
   } pf;
+  bool pf_mismatch = false;   // W > 1: the lookup consumed a prefetched step with other arguments
+  uint32_t late_err_bits = 0; // W > 1: error bits the step's gradient signal must still carry
   int32_t *blen = nullptr;
   SortWorkspace sws{};
   double *partials = nullptr;
@@ -119,6 +122,10 @@ struct emb_ctx {
   uint32_t *inv = nullptr;           // [max_ids] occurrence -> o*cap + sendpos
   uint32_t *outidx = nullptr;        // [max_ids] sorted position -> sendpos
   int64_t *scnt = nullptr;           // [P2P_MAXW] my per-owner counts (device)
+  // (the three above point into set epoch & 1 of these, like skey / spay into sk_set / sp_set: a
+  // prefetched first phase of step e + 1 writes the set step e's backward does not read)
+  uint32_t *inv_set[2] = {nullptr, nullptr}, *outidx_set[2] = {nullptr, nullptr};
+  int64_t *scnt_set[2] = {nullptr, nullptr};
   uint32_t *route_tot = nullptr, *route_counter = nullptr, *route_done = nullptr;
   uint64_t *route_status = nullptr;
   uint32_t route_tag = 0;
@@ -144,7 +151,7 @@ struct emb_ctx {
 
   // ---- streams / step state
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_pf = nullptr, ev_phase = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_pf = nullptr, ev_phase = nullptr, ev_pfdone = nullptr;
   int state = 0;  // 0 idle, 1 looked up
   int32_t batch = 0;
   int64_t nnz = 0;
@@ -507,6 +514,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_pf, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_phase, cudaEventDisableTiming));
+  CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_pfdone, cudaEventDisableTiming));
   CUDA_TRY(h, launch_init(h->w, h->a, h->opt == EMB_OPT_ROWWISE_ADAGRAD, h->rows_local, h->D, h->seed,
                           h->init_accum, ks, h->rank, h->side));
 
@@ -528,10 +536,8 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
   bad |= dalloc(h, &h->k0, N) != cudaSuccess;
   bad |= dalloc(h, &h->v0, N) != cudaSuccess;
   bad |= dalloc(h, &h->sort_scratch, N) != cudaSuccess;
-  if (W == 1) {
-    bad |= dalloc(h, &h->sk_set[1], N) != cudaSuccess;
-    bad |= dalloc(h, &h->sp_set[1], N) != cudaSuccess;
-  }
+  bad |= dalloc(h, &h->sk_set[1], N) != cudaSuccess;
+  bad |= dalloc(h, &h->sp_set[1], N) != cudaSuccess;
   bad |= dalloc(h, &h->k1, N) != cudaSuccess;
   bad |= dalloc(h, &h->v1, N) != cudaSuccess;
   bad |= dalloc(h, &h->blen, SB) != cudaSuccess;
@@ -549,9 +555,14 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
   bad |= dalloc(h, &h->fin, 3) != cudaSuccess;
   bad |= dalloc(h, &h->err_dev, 1) != cudaSuccess;
   if (W > 1) {
-    bad |= dalloc(h, &h->inv, N) != cudaSuccess;
-    bad |= dalloc(h, &h->outidx, N) != cudaSuccess;
-    bad |= dalloc(h, &h->scnt, P2P_MAXW) != cudaSuccess;
+    for (int k = 0; k < 2; ++k) {
+      bad |= dalloc(h, &h->inv_set[k], N) != cudaSuccess;
+      bad |= dalloc(h, &h->outidx_set[k], N) != cudaSuccess;
+      bad |= dalloc(h, &h->scnt_set[k], P2P_MAXW) != cudaSuccess;
+    }
+    h->inv = h->inv_set[0];
+    h->outidx = h->outidx_set[0];
+    h->scnt = h->scnt_set[0];
     bad |= dalloc(h, &h->route_tot, P2P_MAXW) != cudaSuccess;
     bad |= dalloc(h, &h->route_counter, 1) != cudaSuccess;
     bad |= dalloc(h, &h->route_done, 1) != cudaSuccess;
@@ -647,7 +658,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
     CUDA_TRY(h, cudaMemset(h->route_done, 0, sizeof(uint32_t)));
     CUDA_TRY(h, cudaMemset(h->route_status, 0,
                            sizeof(uint64_t) * std::max<size_t>(route_status_words(N), (size_t)(EMB_MAX_SLOTS * 32 + 1) * P2P_MAXW)));
-    CUDA_TRY(h, cudaMemset(h->scnt, 0, sizeof(int64_t) * P2P_MAXW));
+    for (int k = 0; k < 2; ++k) CUDA_TRY(h, cudaMemset(h->scnt_set[k], 0, sizeof(int64_t) * P2P_MAXW));
     CUDA_TRY(h, cudaMemset(h->n_merged, 0, sizeof(int64_t)));
     CUDA_TRY(h, cudaMemset(h->xmat, 0, sizeof(int64_t) * 4 * P2P_MAXW));
     CUDA_TRY(h, cudaMemset(h->flags, 0, sizeof(uint64_t) * P2P_NKIND * P2P_MAXW));
@@ -677,7 +688,7 @@ void destroy_impl(emb_ctx *h) {
   for (void *p : h->allocs) cudaFree(p);
   if (h->err_host) cudaFreeHost(h->err_host);
   for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
-  for (cudaEvent_t e : {h->ev_fork, h->ev_join, h->ev_pf, h->ev_phase})
+  for (cudaEvent_t e : {h->ev_fork, h->ev_join, h->ev_pf, h->ev_phase, h->ev_pfdone})
     if (e) cudaEventDestroy(e);
   for (int k = 0; k < 2; ++k)
     for (cudaEvent_t e : {h->ev_h2d[k], h->ev_h2d2[k], h->ev_looked[k], h->ev_d2h[k], h->ev_free[k]})
@@ -724,13 +735,44 @@ SegSortArgs segsort_args(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   return sa;
 }
 
+emb_status_t launch_l0(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz,
+                       uint64_t e, uint32_t extra_err, cudaStream_t st);
+
+// W > 1: run the first phase (dedup sort + route, raises KEYS) of the NEXT step now, on the side
+// stream, so it overlaps the pending backward. It writes buffer set (epoch + 1) & 1; the next lookup
+// consumes it (lookup_phase0). It cannot be withdrawn once its keys are on their way to the owners:
+// a lookup with other arguments takes part in the step with an empty batch and fails it everywhere.
+emb_status_t prefetch_w2(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz,
+                         cudaStream_t st) {
+  if (h->pf.valid)
+    return fail(h, EMB_ERR_STATE, "prefetch: a prefetched step is already pending (world > 1: the next emb_lookup "
+                                  "consumes it)");
+  if (!h->segsort_ok || batch == 0 || nnz == 0) return EMB_OK;  // the lookup runs its own first phase
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  CUDA_TRY(h, cudaEventRecord(h->ev_pf, st));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_pf, 0));
+  const uint64_t e = h->epoch + 1;
+  emb_status_t s = launch_l0(h, ids, offsets, batch, nnz, e, 0u, h->side);
+  if (s != EMB_OK) return s;
+  CUDA_TRY(h, cudaEventRecord(h->ev_pfdone, h->side));
+  h->pf.valid = true;
+  h->pf.ids = ids;
+  h->pf.offsets = offsets;
+  h->pf.batch = batch;
+  h->pf.nnz = nnz;
+  h->pf.set = (int)(e & 1u);
+  h->pf.epoch = e;
+  return EMB_OK;
+}
+
 emb_status_t lookup_prefetch_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                                   int64_t nnz, cudaStream_t st) {
   if (batch < 0 || batch > h->max_batch || nnz < 0 || nnz > h->max_ids || (batch == 0 && nnz != 0))
     return fail(h, EMB_ERR_INVALID, "prefetch: batch / nnz out of range");
   if ((batch > 0 && !offsets) || (nnz > 0 && !ids)) return fail(h, EMB_ERR_INVALID, "prefetch: NULL ids/offsets");
+  if (h->world > 1) return prefetch_w2(h, ids, offsets, batch, nnz, st);
   h->pf.valid = false;
-  if (h->world != 1 || !h->segsort_ok || batch == 0 || nnz == 0) return EMB_OK;  // nothing to overlap
+  if (!h->segsort_ok || batch == 0 || nnz == 0) return EMB_OK;  // nothing to overlap
   CUDA_TRY(h, cudaSetDevice(h->device));
   // ordered after everything already on the caller stream (the inputs, the current lookup), not after
   // the backward the caller enqueues next: the sort of step k+1 overlaps the gradient pass of step k.
@@ -852,24 +894,38 @@ emb_status_t lookup_w1(emb_ctx *h, const int64_t *ids, const int64_t *offsets, i
 }
 
 // ---- world > 1 phases (see the file header). The step's arguments are in h (cur_*, batch, nnz).
-// L0: dedup sort + route (raises KEYS)
-emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
-  const int64_t *ids = h->cur_ids, *offsets = h->cur_offsets;
-  const int32_t batch = h->batch;
-  const int64_t nnz = h->nnz;
-  h->epoch += 1;
-  h->p2p.epoch = h->epoch;
-  h->skey = h->k0;
-  h->spay = h->v0;
+constexpr const char *PF_MISMATCH_MSG =
+    "emb_lookup arguments differ from the pending emb_lookup_prefetch (the rank took part with an empty batch; the "
+    "step updates nothing on any rank)";
+
+// make step e current: its epoch and its buffer set (e & 1)
+void begin_step(emb_ctx *h, uint64_t e) {
+  const int set = (int)(e & 1u);
+  h->epoch = e;
+  h->p2p.epoch = e;
+  h->skey = h->sk_set[set];
+  h->spay = h->sp_set[set];
+  h->inv = h->inv_set[set];
+  h->outidx = h->outidx_set[set];
+  h->scnt = h->scnt_set[set];
+}
+
+// L0 of the step with epoch e: dedup sort + route into buffer set e & 1 (raises KEYS(e)). Only the
+// per-table sort path writes the set buffers; the general radix path (never prefetched) leaves its
+// sorted keys in h->skey / h->spay.
+emb_status_t launch_l0(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz,
+                       uint64_t e, uint32_t extra_err, cudaStream_t st) {
+  const int set = (int)(e & 1u);
   RouteArgs ra{};
-  ra.skey = h->skey;
-  ra.spay = h->spay;
+  ra.skey = h->sk_set[set];
+  ra.spay = h->sp_set[set];
   ra.n = (batch > 0) ? nnz : 0;
   ra.ks = h->ks;
   ra.p2p = h->p2p;
-  ra.outidx = h->outidx;
-  ra.inv = h->inv;
-  ra.scnt = h->scnt;
+  ra.p2p.epoch = e;
+  ra.outidx = h->outidx_set[set];
+  ra.inv = h->inv_set[set];
+  ra.scnt = h->scnt_set[set];
   ra.tot = h->route_tot;
   ra.status = h->route_status;
   ra.counter = h->route_counter;
@@ -877,12 +933,12 @@ emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
   if (++h->route_tag == 0) h->route_tag = 1;
   ra.tag = h->route_tag;
   ra.err = h->err_dev;
-  ra.extra_err = h->step_err_bits;
+  ra.extra_err = extra_err;
   static int fuse = -1;  // experiment knob EMB_FUSED_ROUTE=0: separate k_route after the per-table sort
   if (fuse < 0) fuse = getenv("EMB_FUSED_ROUTE") ? atoi(getenv("EMB_FUSED_ROUTE")) : 1;
   if (batch > 0 && nnz > 0) {
     if (h->segsort_ok) {
-      SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, 0);
+      SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, set);
       sa.validate = 1;
       if (fuse) {  // the route runs in the sort's epilogue (no separate launch)
         sa.route = 1;
@@ -894,9 +950,9 @@ emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
     } else {
       LAUNCH(h, KID_KEYS, st, launch_keys(keys_args(h, ids, offsets, batch, nnz), st));
       int nl = 0;
-      cudaError_t e = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz, h->ks.key_bits,
+      cudaError_t r = radix_sort_pairs(h->sws, h->key_csr, nullptr, h->k0, h->v0, h->k1, h->v1, nnz, h->ks.key_bits,
                                        st, &h->skey, &h->spay, &nl, prof_hook, h);
-      if (e != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+      if (r != cudaSuccess) return fail(h, EMB_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(r));
       h->launches += nl;
       ra.skey = h->skey;
       ra.spay = h->spay;
@@ -906,6 +962,29 @@ emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
   }
   LAUNCH(h, KID_ROUTE, st, launch_route(ra, st));
   return EMB_OK;
+}
+
+// L0: dedup sort + route (raises KEYS), or consume the first phase a prefetch already ran
+emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
+  h->pf_mismatch = false;
+  if (h->pf.valid) {
+    h->pf.valid = false;
+    const bool match = h->step_err_bits == 0 && h->pf.ids == h->cur_ids && h->pf.offsets == h->cur_offsets &&
+                       h->pf.batch == h->batch && h->pf.nnz == h->nnz;
+    begin_step(h, h->pf.epoch);
+    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_pfdone, 0));
+    if (!match) {  // the owners already hold the prefetched keys: take part empty, fail the step everywhere
+      h->pf_mismatch = true;
+      h->late_err_bits = EMB_DEVERR_INVALID;
+      h->batch = 0;
+      h->nnz = 0;
+      h->cur_out = nullptr;
+      LAUNCH(h, KID_SIGNAL, st, launch_mark_err(h->err_dev, EMB_DEVERR_INVALID, st));  // sticky, as a lookup argument error
+    }
+    return EMB_OK;
+  }
+  begin_step(h, h->epoch + 1);
+  return launch_l0(h, h->cur_ids, h->cur_offsets, h->batch, h->nnz, h->epoch, h->step_err_bits, st);
 }
 
 // L1: wait KEYS -> owner merge (side stream) | gather + push the requested rows (raises ROWS)
@@ -990,7 +1069,9 @@ emb_status_t backward_phase0(emb_ctx *h, const float *d_out, double lr, cudaStre
   if (h->batch > 0 && h->nnz > 0 && d_out)
     LAUNCH(h, KID_GRAD_PUSH, st, launch_grad(g, st));
   else
-    LAUNCH(h, KID_SIGNAL, st, launch_signal(h->p2p, P2P_GRADS, d_out || h->batch == 0 ? 0u : EMB_DEVERR_INVALID, st));
+    LAUNCH(h, KID_SIGNAL, st, launch_signal(h->p2p, P2P_GRADS, (d_out || h->batch == 0 ? 0u : EMB_DEVERR_INVALID) |
+                                                                  h->late_err_bits, st));
+  h->late_err_bits = 0;
   return EMB_OK;
 }
 
@@ -1053,6 +1134,7 @@ emb_status_t lookup_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
   h->state = 1;
   if (*ae) return fail(h, EMB_ERR_INVALID, std::string(ae) + " (the rank took part with an empty batch; the step "
                                                               "updates nothing on any rank)");
+  if (h->pf_mismatch) return fail(h, EMB_ERR_INVALID, PF_MISMATCH_MSG);
   return check_sticky(h);
 }
 
@@ -1279,7 +1361,23 @@ emb_status_t emb_lookup(emb_handle_t h, const int64_t *ids, const int64_t *offse
 emb_status_t emb_lookup_prefetch(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                                  int64_t nnz, void *cuda_stream) {
   if (!h) return EMB_ERR_INVALID;
+  if (h->group && h->world > 1) return fail(h, EMB_ERR_STATE, "a group handle prefetches through emb_lookup_prefetch_group");
   return lookup_prefetch_impl(h, ids, offsets, batch, nnz, static_cast<cudaStream_t>(cuda_stream));
+}
+
+emb_status_t emb_lookup_prefetch_group(emb_handle_t *hs, int32_t n, const int64_t *const *ids,
+                                       const int64_t *const *offsets, const int32_t *batch, const int64_t *nnz,
+                                       void *const *streams) {
+  if (check_group(hs, n) != EMB_OK || !ids || !offsets || !batch || !nnz) return EMB_ERR_INVALID;
+  // every rank's first phase only raises flags (no waits), so the ranks' prefetches need no ordering
+  // among themselves; the next emb_lookup_group orders its second phase after all of them
+  emb_status_t first_err = EMB_OK;
+  for (int r = 0; r < n; ++r) {
+    emb_status_t s = lookup_prefetch_impl(hs[r], ids[r], offsets[r], batch[r], nnz[r],
+                                          static_cast<cudaStream_t>(streams ? streams[r] : nullptr));
+    if (s != EMB_OK && first_err == EMB_OK) first_err = s;
+  }
+  return first_err;
 }
 
 emb_status_t emb_backward_update(emb_handle_t h, const float *d_out, double lr, void *cuda_stream) {
@@ -1334,6 +1432,8 @@ emb_status_t emb_lookup_group(emb_handle_t *hs, int32_t n, const int64_t *const 
   if (s != EMB_OK) return s;
   for (int r = 0; r < n; ++r) hs[r]->state = 1;
   if (first_err != EMB_OK) return first_err;
+  for (int r = 0; r < n; ++r)
+    if (hs[r]->pf_mismatch) return fail(hs[r], EMB_ERR_INVALID, std::string("rank ") + std::to_string(r) + ": " + PF_MISMATCH_MSG);
   for (int r = 0; r < n; ++r) {
     emb_status_t e = check_sticky(hs[r]);
     if (e != EMB_OK) return e;

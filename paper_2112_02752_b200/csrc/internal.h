@@ -81,6 +81,8 @@ cudaError_t launch_wait(const P2PArgs &a, int kind, uint64_t epoch, uint32_t *er
 // raise `kind` in every peer (a producer with nothing to do); err_bits != 0 are first OR-ed into every
 // owner's error slot of this step (xmat[parity][1][rank]): the owners then skip the update
 cudaError_t launch_signal(const P2PArgs &a, int kind, uint32_t err_bits, cudaStream_t st);
+// OR `bits` into the sticky device error word
+cudaError_t launch_mark_err(uint32_t *err, uint32_t bits, cudaStream_t st);
 // owner (A6 + X2 fused): for every source s != rank and i < xmat[s] (keys received from s this step),
 // the table row of local id recv_keys[s*cap + i] is stored straight into requester s's row region for
 // this owner, peer_uniq_rows[s][rank*cap + i] (peer stores over NVLink); the last block raises ROWS.

@@ -38,6 +38,13 @@ cudaError_t launch_signal(const P2PArgs &a, int kind, uint32_t err_bits, cudaStr
   return cudaGetLastError();
 }
 
+// OR bits into the sticky device error word (a host-detected error of an already routed step)
+__global__ void k_mark_err(uint32_t *err, uint32_t bits) { atomicOr(err, bits); }
+cudaError_t launch_mark_err(uint32_t *err, uint32_t bits, cudaStream_t st) {
+  k_mark_err<<<1, 1, 0, st>>>(err, bits);
+  return cudaGetLastError();
+}
+
 // wait for flag `kind` == epoch from every source
 __global__ void k_wait(P2PArgs a, int kind, uint64_t epoch, uint32_t *err) {
   if (threadIdx.x == 0) p2p_spin(a, kind, epoch, err);

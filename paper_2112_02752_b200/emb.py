@@ -28,7 +28,8 @@ SHARD = {"cyclic": 0, "block": 1}
 # every symbol include/emb.h declares (checked by tests/test_abi.py)
 EXPORTED = [
     "emb_create", "emb_create_group", "emb_destroy", "emb_get_unique_id", "emb_lookup", "emb_lookup_prefetch",
-    "emb_backward_update", "emb_lookup_group", "emb_backward_update_group", "emb_lookup_host", "emb_host_sync",
+    "emb_backward_update", "emb_lookup_group", "emb_backward_update_group", "emb_lookup_prefetch_group",
+    "emb_lookup_host", "emb_host_sync",
     "emb_backward_update_host", "emb_read_rows", "emb_write_rows", "emb_last_step_info", "emb_last_unique",
     "emb_last_owner_unique", "emb_rows_local", "emb_profile_enable", "emb_profile_reset", "emb_profile_read",
     "emb_profile_name", "emb_clear_error", "emb_last_error",
@@ -83,6 +84,9 @@ def lib() -> ctypes.CDLL:
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(vp),
                                    ctypes.POINTER(vp)]
     L.emb_backward_update_group.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(vp), ctypes.c_double,
+                                            ctypes.POINTER(vp)]
+    L.emb_lookup_prefetch_group.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                            ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
                                             ctypes.POINTER(vp)]
     L.emb_destroy.argtypes = [vp]
     L.emb_get_unique_id.argtypes = [vp]
@@ -337,6 +341,15 @@ class EmbeddingGroup:
                                     (ctypes.c_void_p * W)(*[_ptr(x) for x in out]), self._streams(streams))
         if st != EMB_OK:
             raise EmbError(st, "emb_lookup_group: " + "; ".join(l.last_error() for l in self.layers))
+
+    def lookup_prefetch(self, ids, offsets, batch, nnz, streams=None):
+        W = self.world
+        st = lib().emb_lookup_prefetch_group(self._hs, W, (ctypes.c_void_p * W)(*[_ptr(x) for x in ids]),
+                                             (ctypes.c_void_p * W)(*[_ptr(x) for x in offsets]),
+                                             (ctypes.c_int32 * W)(*[int(b) for b in batch]),
+                                             (ctypes.c_int64 * W)(*[int(n) for n in nnz]), self._streams(streams))
+        if st != EMB_OK:
+            raise EmbError(st, "emb_lookup_prefetch_group: " + "; ".join(l.last_error() for l in self.layers))
 
     def backward_update(self, d_out, lr: float, streams=None):
         W = self.world

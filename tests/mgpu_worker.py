@@ -26,6 +26,8 @@ def main():
     nid = D.share_unique_id(E.get_unique_id)
     case = os.environ.get("EMB_MGPU_CASE", "c3")
     shard = os.environ.get("EMB_MGPU_SHARD", "cyclic")
+    # EMB_MGPU_PREFETCH=1: the next step's first phase (sort + route) is prefetched before each backward
+    prefetch = os.environ.get("EMB_MGPU_PREFETCH", "0") == "1"
     wl, B, steps = C.case_workload(case, world)
     cfgW = O.config_from_workload(wl, world=world, shard=shard)
     cfg1 = O.config_from_workload(wl, world=1)
@@ -34,6 +36,7 @@ def main():
                        world=world, rank=rank, nccl_id=nid, device=local, shard=shard)
     ora = O.OracleEmbedding(cfg1)
     msgs = []
+    dbs = [DeviceBatch(bts[s][rank], wl.num_slots, wl.dim, local) for s in range(steps)]
     for s in range(steps):
         batches = bts[s]
         mine, t_of = C.owned_touched(cfg1, cfgW, batches, rank)
@@ -43,7 +46,7 @@ def main():
         for gk, gw_, ga in gathered:
             if gk.size:
                 ora.load_rows(gk, gw_, ga)
-        db = DeviceBatch(batches[rank], wl.num_slots, wl.dim, local)
+        db = dbs[s]
         layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out)
         torch.cuda.synchronize()
         info = layer.step_info()
@@ -54,6 +57,9 @@ def main():
         dist.all_gather_object(sends, info["send_counts"])
         C.check_rank_step(msgs, s, rank, cfgW, ora, batches, db.out.cpu().numpy(), Yo, info, keys, counts, okeys,
                           fanin, [sends[q][rank] for q in range(world)])
+        if prefetch and s + 1 < steps:
+            nx = dbs[s + 1]
+            layer.lookup_prefetch(nx.ids, nx.offsets, nx.batch, nx.nnz)
         layer.backward_update(db.dy, wl.lr)
         torch.cuda.synchronize()
         ora.backward_update([b.dy for b in batches], wl.lr)

@@ -35,7 +35,7 @@ def _step(grp, dbs, lr, torch):
     torch.cuda.synchronize()
 
 
-def _run_group(torch, case, world, shard="cyclic", devices=None):
+def _run_group(torch, case, world, shard="cyclic", devices=None, prefetch=False):
     from paper_2112_02752_b200.harness import make_group
     devices = devices or [0] * world
     wl, B, steps = C.case_workload(case, world)
@@ -46,6 +46,7 @@ def _run_group(torch, case, world, shard="cyclic", devices=None):
     grp = make_group(wl, world=world, max_batch=B + 16 * world, max_ids=max_ids, devices=devices, shard=shard)
     ora = O.OracleEmbedding(cfg1)
     msgs = []
+    all_dbs = [_device_batches(bts[s], wl, devices) for s in range(steps)]
     try:
         for s in range(steps):
             batches = bts[s]
@@ -54,7 +55,7 @@ def _run_group(torch, case, world, shard="cyclic", devices=None):
                 mine, t_of = owned[r]
                 if mine.size:
                     ora.load_rows(mine, *C.read_owned(grp.layers[r], cfg1, mine, t_of, wl.dim))
-            dbs = _device_batches(batches, wl, devices)
+            dbs = all_dbs[s]
             _step(grp, dbs, wl.lr, torch)
             Yo = ora.lookup([(b.ids, b.offsets, b.batch) for b in batches])
             infos = [l.step_info() for l in grp.layers]
@@ -64,6 +65,10 @@ def _run_group(torch, case, world, shard="cyclic", devices=None):
                 okeys, fanin = lay.last_owner_unique()
                 C.check_rank_step(msgs, s, r, cfgW, ora, batches, dbs[r].out.cpu().numpy(), Yo[r], infos[r], keys,
                                   counts, okeys, fanin, [infos[q]["send_counts"][r] for q in range(world)])
+            if prefetch and s + 1 < steps:  # the next step's sort + route overlaps this backward
+                nx = all_dbs[s + 1]
+                grp.lookup_prefetch([d.ids for d in nx], [d.offsets for d in nx], [d.batch for d in nx],
+                                    [d.nnz for d in nx])
             grp.backward_update([d.dy for d in dbs], wl.lr)
             torch.cuda.synchronize()
             ora.backward_update([b.dy for b in batches], wl.lr)
@@ -90,6 +95,82 @@ def _run_group(torch, case, world, shard="cyclic", devices=None):
     ("c3", 8, "cyclic"), ("hot", 8, "block"), ("gen", 8, "cyclic"), ("c3rw", 8, "cyclic"), ("c3", 16, "cyclic")])
 def test_group_row_sharded_parity(torch, case, world, shard):
     _run_group(torch, case, world, shard)
+
+
+@pytest.mark.parametrize("case,world,shard", [
+    ("c3", 2, "cyclic"), ("c3", 4, "block"), ("hot", 3, "cyclic"), ("c3rw", 2, "cyclic"), ("edge", 2, "cyclic"),
+    ("edge", 4, "block"), ("gen", 2, "cyclic"), ("c3full", 2, "cyclic"), ("c3", 8, "cyclic")])
+def test_group_prefetch_parity(torch, case, world, shard):
+    """emb_lookup_prefetch_group before every backward: the next step's sort + route (keys already in
+    the owners' regions, buffer set epoch & 1) overlaps this step's gradient passes; results as without."""
+    _run_group(torch, case, world, shard, prefetch=True)
+
+
+def test_group_prefetch_mismatch_and_state(torch):
+    """A lookup whose arguments differ from the pending prefetch takes part with an empty batch and fails
+    the step on every rank (no row changes anywhere); a second prefetch before the lookup is a state
+    error; afterwards plain and prefetched steps match the oracle again."""
+    from paper_2112_02752_b200.emb import EmbError, EMB_ERR_INVALID, EMB_ERR_STATE
+    from paper_2112_02752_b200.harness import make_group
+    W = 2
+    wl = synthgen.WORKLOADS["C3"].with_(rows=(4000, 3000), slot_table=(0, 1), dim=16, opt="adagrad")
+    cfgW = O.config_from_workload(wl, world=W)
+    cfg1 = O.config_from_workload(wl, world=1)
+    B = 64
+    bts = [[synthgen.make_batch(wl, rank=r, step=s, batch=B) for r in range(W)] for s in range(4)]
+    grp = make_group(wl, world=W, max_batch=B, max_ids=max(b.nnz for st in bts for b in st))
+    try:
+        all_rows = [np.arange(O.rows_local(cfgW, r)) for r in range(W)]
+
+        def snapshot():
+            out = []
+            for r in range(W):
+                g = all_rows[r] * W + r  # cyclic: local -> global
+                t = np.searchsorted(cfg1.base, g, side="right") - 1
+                out.append(C.read_owned(grp.layers[r], cfg1, g, t, wl.dim))
+            return out
+
+        dbs = [_device_batches(bts[s], wl, [0] * W) for s in range(4)]
+        before = snapshot()
+        # prefetch step 0's batches, then look up with rank 1's step-1 batch instead
+        grp.lookup_prefetch([d.ids for d in dbs[0]], [d.offsets for d in dbs[0]], [d.batch for d in dbs[0]],
+                            [d.nnz for d in dbs[0]])
+        with pytest.raises(EmbError) as ei:
+            grp.lookup_prefetch([d.ids for d in dbs[0]], [d.offsets for d in dbs[0]], [d.batch for d in dbs[0]],
+                                [d.nnz for d in dbs[0]])
+        assert ei.value.status == EMB_ERR_STATE
+        mixed = [dbs[0][0], dbs[1][1]]
+        with pytest.raises(EmbError) as ei:
+            _step(grp, mixed, wl.lr, torch)
+        assert ei.value.status == EMB_ERR_INVALID
+        with pytest.raises(EmbError):
+            grp.backward_update([d.dy for d in mixed], wl.lr)
+        torch.cuda.synchronize()
+        after = snapshot()
+        for r in range(W):
+            assert np.array_equal(before[r][0], after[r][0]) and np.array_equal(before[r][1], after[r][1]), \
+                f"rank {r} changed rows in an aborted step"
+        for r in range(W):
+            grp.layers[r].clear_error()
+        # steps 2 (plain) and 3 (prefetched during step 2's backward) match the oracle
+        ora = O.OracleEmbedding(cfg1)
+        for s in (2, 3):
+            _step(grp, dbs[s], wl.lr, torch)
+            Yo = ora.lookup([(b.ids, b.offsets, b.batch) for b in bts[s]])
+            for r in range(W):
+                assert C.close(dbs[s][r].out.cpu().numpy(), Yo[r]), f"step {s} rank {r}: Y mismatch"
+            if s == 2:
+                grp.lookup_prefetch([d.ids for d in dbs[3]], [d.offsets for d in dbs[3]], [d.batch for d in dbs[3]],
+                                    [d.nnz for d in dbs[3]])
+            grp.backward_update([d.dy for d in dbs[s]], wl.lr)
+            torch.cuda.synchronize()
+            ora.backward_update([b.dy for b in bts[s]], wl.lr)
+            for r in range(W):
+                mine, t_of = C.owned_touched(cfg1, cfgW, bts[s], r)
+                w, a = C.read_owned(grp.layers[r], cfg1, mine, t_of, wl.dim)
+                assert C.close(w, ora.rows(mine)[0]) and C.close(a, ora.rows(mine)[1]), f"step {s} rank {r}"
+    finally:
+        grp.close()
 
 
 def test_group_on_distinct_devices(torch):
