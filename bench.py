@@ -397,6 +397,9 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
             fwd_ev[i][0].record(stream)
             layer.lookup(db.ids, db.offsets, db.batch, db.nnz, db.out, stream)
             fwd_ev[i][1].record(stream)
+            if os.environ.get("EMB_BENCH_PROFILE_PREFETCH") == "1" and use_prefetch and i < profile_steps - 1:
+                nx = dev_batches[(i + 1) % nstage]  # (diagnostics: the timed loop's overlap, profiled)
+                layer.lookup_prefetch(nx.ids, nx.offsets, nx.batch, nx.nnz, stream)
             layer.backward_update(db.dy, wl.lr, stream)
         torch.cuda.synchronize()
         prof = layer.profile_read()

@@ -145,18 +145,19 @@ emb_status_t emb_lookup(emb_handle_t h, const int64_t *ids, const int64_t *offse
                         int64_t nnz, float *out, void *cuda_stream);
 
 /* Optional pipelining (per-table sort path, i.e. a monotone slot -> table map; a no-op returning
- * EMB_OK otherwise or for an empty batch): start the first part of the NEXT emb_lookup on the library's
- * internal stream, ordered after the work already enqueued on cuda_stream (so the inputs must be ready
- * there) but not after work enqueued later. Called between emb_lookup(k) and emb_backward_update(k),
- * it overlaps the gradient pass of step k. Results are identical with or without it.
+ * EMB_OK otherwise or for an empty batch): declare the NEXT emb_lookup's inputs, ready on cuda_stream
+ * at this call. Called between emb_lookup(k) and emb_backward_update(k), the first part of lookup k+1
+ * is launched by emb_backward_update(k) right after its gradient kernel (on a lowest-priority library
+ * stream) and overlaps the gradient pass. Results are identical with or without it.
  *  - world == 1: the per-table dedup sort. The next emb_lookup consumes it when called with the same
  *    ids / offsets pointers and batch / nnz; any other call discards it.
- *  - world > 1: the dedup sort AND the route: the step's distinct keys are stored into their owners'
- *    receive regions (the prefetch is the first phase of the next collective step, so it cannot be
- *    withdrawn). The next emb_lookup must pass the same ids / offsets pointers and batch / nnz; if it
- *    does not, it returns EMB_ERR_INVALID after taking part with an empty batch and the step updates
- *    nothing on any rank. A second prefetch before that lookup returns EMB_ERR_STATE. Ranks may mix
- *    prefetching and plain lookups freely. Group handles use emb_lookup_prefetch_group.
+ *  - world > 1: the dedup sort AND the route (the step's distinct keys are stored into their owners'
+ *    receive regions: the first phase of the next collective step, which cannot be withdrawn once
+ *    launched). The next emb_lookup must then pass the same ids / offsets pointers and batch / nnz;
+ *    if it does not, it returns EMB_ERR_INVALID after taking part with an empty batch and the step
+ *    updates nothing on any rank. A second prefetch before that lookup returns EMB_ERR_STATE. Ranks
+ *    may mix prefetching and plain lookups freely. Group handles use emb_lookup_prefetch_group.
+ * A request followed by emb_lookup without a backward in between launched nothing and is dropped.
  * ids and offsets must stay valid and unmodified until the consuming emb_lookup. */
 emb_status_t emb_lookup_prefetch(emb_handle_t h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                                  int64_t nnz, void *cuda_stream);

@@ -94,6 +94,7 @@ struct emb_ctx {
     int64_t nnz = 0;
     int set = 0;
     uint64_t epoch = 0;  // W > 1: the step whose first phase (sort + route) the prefetch ran
+    bool requested = false;  // recorded by emb_lookup_prefetch, launched by the next backward
   } pf;
   bool pf_mismatch = false;   // W > 1: the lookup consumed a prefetched step with other arguments
   uint32_t late_err_bits = 0; // W > 1: error bits the step's gradient signal must still carry
@@ -151,7 +152,9 @@ struct emb_ctx {
 
   // ---- streams / step state
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_pf = nullptr, ev_phase = nullptr, ev_pfdone = nullptr;
+  cudaStream_t side_lo = nullptr;  // lowest priority: prefetched work (launch_prefetch)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_pf = nullptr, ev_phase = nullptr, ev_pfdone = nullptr,
+              ev_pre = nullptr;  // ev_pre: on the caller stream right before the backward's gradient kernel
   int state = 0;  // 0 idle, 1 looked up
   int32_t batch = 0;
   int64_t nnz = 0;
@@ -515,6 +518,7 @@ emb_status_t create_impl(const emb_config_t *cfg, emb_ctx *h, int64_t group_cap)
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_pf, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_phase, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_pfdone, cudaEventDisableTiming));
+  CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_pre, cudaEventDisableTiming));
   CUDA_TRY(h, launch_init(h->w, h->a, h->opt == EMB_OPT_ROWWISE_ADAGRAD, h->rows_local, h->D, h->seed,
                           h->init_accum, ks, h->rank, h->side));
 
@@ -688,12 +692,12 @@ void destroy_impl(emb_ctx *h) {
   for (void *p : h->allocs) cudaFree(p);
   if (h->err_host) cudaFreeHost(h->err_host);
   for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
-  for (cudaEvent_t e : {h->ev_fork, h->ev_join, h->ev_pf, h->ev_phase, h->ev_pfdone})
+  for (cudaEvent_t e : {h->ev_fork, h->ev_join, h->ev_pf, h->ev_phase, h->ev_pfdone, h->ev_pre})
     if (e) cudaEventDestroy(e);
   for (int k = 0; k < 2; ++k)
     for (cudaEvent_t e : {h->ev_h2d[k], h->ev_h2d2[k], h->ev_looked[k], h->ev_d2h[k], h->ev_free[k]})
       if (e) cudaEventDestroy(e);
-  for (cudaStream_t q : {h->side, h->h2d_stream, h->d2h_stream})
+  for (cudaStream_t q : {h->side, h->side_lo, h->h2d_stream, h->d2h_stream})
     if (q) cudaStreamDestroy(q);
   delete h;
 }
@@ -738,56 +742,70 @@ SegSortArgs segsort_args(emb_ctx *h, const int64_t *ids, const int64_t *offsets,
 emb_status_t launch_l0(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz,
                        uint64_t e, uint32_t extra_err, cudaStream_t st);
 
-// W > 1: run the first phase (dedup sort + route, raises KEYS) of the NEXT step now, on the side
-// stream, so it overlaps the pending backward. It writes buffer set (epoch + 1) & 1; the next lookup
-// consumes it (lookup_phase0). It cannot be withdrawn once its keys are on their way to the owners:
-// a lookup with other arguments takes part in the step with an empty batch and fails it everywhere.
-emb_status_t prefetch_w2(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz,
-                         cudaStream_t st) {
-  if (h->pf.valid)
-    return fail(h, EMB_ERR_STATE, "prefetch: a prefetched step is already pending (world > 1: the next emb_lookup "
-                                  "consumes it)");
-  if (!h->segsort_ok || batch == 0 || nnz == 0) return EMB_OK;  // the lookup runs its own first phase
-  CUDA_TRY(h, cudaSetDevice(h->device));
-  CUDA_TRY(h, cudaEventRecord(h->ev_pf, st));
-  CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_pf, 0));
-  const uint64_t e = h->epoch + 1;
-  emb_status_t s = launch_l0(h, ids, offsets, batch, nnz, e, 0u, h->side);
-  if (s != EMB_OK) return s;
-  CUDA_TRY(h, cudaEventRecord(h->ev_pfdone, h->side));
-  h->pf.valid = true;
-  h->pf.ids = ids;
-  h->pf.offsets = offsets;
-  h->pf.batch = batch;
-  h->pf.nnz = nnz;
-  h->pf.set = (int)(e & 1u);
-  h->pf.epoch = e;
-  return EMB_OK;
-}
+emb_status_t launch_l0(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch, int64_t nnz,
+                       uint64_t e, uint32_t extra_err, cudaStream_t st);
 
+// emb_lookup_prefetch only RECORDS the request (the inputs are ready at ev_pf on the caller stream);
+// the next backward launches it (launch_prefetch) right after its own gradient kernel, on the
+// lowest-priority stream, so the persistent gradient pass's CTAs are resident first and the prefetched
+// work takes SMs as they free up. (Launched at the prefetch call, the per-table sort's CTAs -- one per
+// SM, 192 KB of shared memory each -- were resident first and the static-range gradient pass waited
+// for them: the W = 2 requester pass stretched 75 -> 122 us, and C2 swung between 129 and 146 us/step
+// with the race.) What it launches:
+//  - W = 1: the per-table sort into the sort-output set the pending backward does not read;
+//  - W > 1: the first phase of the NEXT step (sort + route into buffer set (epoch + 1) & 1, raises
+//    KEYS); the next lookup consumes it (lookup_phase0). Once launched it cannot be withdrawn (its
+//    keys are on their way to the owners): a lookup with other arguments then takes part with an
+//    empty batch and fails the step everywhere.
+// A request with no backward before the next lookup is dropped (nothing was launched).
 emb_status_t lookup_prefetch_impl(emb_ctx *h, const int64_t *ids, const int64_t *offsets, int32_t batch,
                                   int64_t nnz, cudaStream_t st) {
   if (batch < 0 || batch > h->max_batch || nnz < 0 || nnz > h->max_ids || (batch == 0 && nnz != 0))
     return fail(h, EMB_ERR_INVALID, "prefetch: batch / nnz out of range");
   if ((batch > 0 && !offsets) || (nnz > 0 && !ids)) return fail(h, EMB_ERR_INVALID, "prefetch: NULL ids/offsets");
-  if (h->world > 1) return prefetch_w2(h, ids, offsets, batch, nnz, st);
-  h->pf.valid = false;
-  if (!h->segsort_ok || batch == 0 || nnz == 0) return EMB_OK;  // nothing to overlap
+  if (h->world > 1 && (h->pf.valid || h->pf.requested))
+    return fail(h, EMB_ERR_STATE, "prefetch: a prefetched step is already pending (world > 1: the next emb_lookup "
+                                  "consumes it)");
+  h->pf.valid = false;  // (W = 1: a new request replaces an older one)
+  h->pf.requested = false;
+  if (!h->segsort_ok || batch == 0 || nnz == 0) return EMB_OK;  // the lookup runs its own first phase
   CUDA_TRY(h, cudaSetDevice(h->device));
-  // ordered after everything already on the caller stream (the inputs, the current lookup), not after
-  // the backward the caller enqueues next: the sort of step k+1 overlaps the gradient pass of step k.
-  // It writes the sort-output set the pending backward does not read.
   CUDA_TRY(h, cudaEventRecord(h->ev_pf, st));
-  CUDA_TRY(h, cudaStreamWaitEvent(h->side, h->ev_pf, 0));
-  const int set = h->cur_set ^ 1;
-  SegSortArgs sa = segsort_args(h, ids, offsets, batch, nnz, set);
-  LAUNCH(h, KID_SORT_PASS, h->side, launch_segsort(sa, h->G, h->side));
-  h->pf.valid = true;
+  h->pf.requested = true;
   h->pf.ids = ids;
   h->pf.offsets = offsets;
   h->pf.batch = batch;
   h->pf.nnz = nnz;
-  h->pf.set = set;
+  return EMB_OK;
+}
+
+// called by the backward right after its gradient kernel: launch a recorded prefetch request
+emb_status_t launch_prefetch(emb_ctx *h) {
+  if (!h->pf.requested) return EMB_OK;
+  h->pf.requested = false;
+  if (!h->side_lo) {
+    int lo_prio = 0, hi_prio = 0;
+    CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->side_lo, cudaStreamNonBlocking, lo_prio));
+  }
+  CUDA_TRY(h, cudaStreamWaitEvent(h->side_lo, h->ev_pf, 0));
+  // ... and not before the gradient kernel is ready (at W > 1 it sits behind a flag wait): ready
+  // together, the gradient kernel (enqueued first, no lower priority) is resident first
+  CUDA_TRY(h, cudaStreamWaitEvent(h->side_lo, h->ev_pre, 0));
+  if (h->world > 1) {
+    const uint64_t e = h->epoch + 1;
+    emb_status_t s = launch_l0(h, h->pf.ids, h->pf.offsets, h->pf.batch, h->pf.nnz, e, 0u, h->side_lo);
+    if (s != EMB_OK) return s;
+    h->pf.set = (int)(e & 1u);
+    h->pf.epoch = e;
+  } else {
+    const int set = h->cur_set ^ 1;
+    SegSortArgs sa = segsort_args(h, h->pf.ids, h->pf.offsets, h->pf.batch, h->pf.nnz, set);
+    LAUNCH(h, KID_SORT_PASS, h->side_lo, launch_segsort(sa, h->G, h->side_lo));
+    h->pf.set = set;
+  }
+  CUDA_TRY(h, cudaEventRecord(h->ev_pfdone, h->side_lo));
+  h->pf.valid = true;
   return EMB_OK;
 }
 
@@ -861,6 +879,7 @@ emb_status_t lookup_w1(emb_ctx *h, const int64_t *ids, const int64_t *offsets, i
   const bool use_pf = h->pf.valid && h->pf.ids == ids && h->pf.offsets == offsets && h->pf.batch == batch &&
                       h->pf.nnz == nnz;
   h->pf.valid = false;
+  h->pf.requested = false;  // (a request no backward launched is dropped)
   if (use_pf) {
     h->cur_set = h->pf.set;
     h->skey = h->sk_set[h->cur_set];
@@ -889,6 +908,7 @@ emb_status_t lookup_w1(emb_ctx *h, const int64_t *ids, const int64_t *offsets, i
   if (batch > 0) LAUNCH(h, KID_POOL, st, launch_pool(pa, st));
   CUDA_TRY(h, cudaEventRecord(h->ev_join, h->side));
   CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_join, 0));
+  if (use_pf) CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_pfdone, 0));  // the prefetched sort (side_lo)
   if (batch > 0 && !fused_pub) LAUNCH(h, KID_KEYS, st, launch_publish_err(h->err_dev, h->err_host_dev, st));
   return EMB_OK;
 }
@@ -967,6 +987,7 @@ emb_status_t launch_l0(emb_ctx *h, const int64_t *ids, const int64_t *offsets, i
 // L0: dedup sort + route (raises KEYS), or consume the first phase a prefetch already ran
 emb_status_t lookup_phase0(emb_ctx *h, cudaStream_t st) {
   h->pf_mismatch = false;
+  h->pf.requested = false;  // (a request no backward launched is dropped: nothing was sent)
   if (h->pf.valid) {
     h->pf.valid = false;
     const bool match = h->step_err_bits == 0 && h->pf.ids == h->cur_ids && h->pf.offsets == h->cur_offsets &&
@@ -1066,13 +1087,14 @@ emb_status_t backward_phase0(emb_ctx *h, const float *d_out, double lr, cudaStre
   g.signal_kind = P2P_GRADS;
   // the owners' "needs lo" bytes (written after their merges, long done by now)
   LAUNCH(h, KID_WAIT, st, launch_wait(h->p2p, P2P_LOF, h->epoch, h->err_dev, st));
+  if (h->pf.requested) CUDA_TRY(h, cudaEventRecord(h->ev_pre, st));
   if (h->batch > 0 && h->nnz > 0 && d_out)
     LAUNCH(h, KID_GRAD_PUSH, st, launch_grad(g, st));
   else
     LAUNCH(h, KID_SIGNAL, st, launch_signal(h->p2p, P2P_GRADS, (d_out || h->batch == 0 ? 0u : EMB_DEVERR_INVALID) |
                                                                   h->late_err_bits, st));
   h->late_err_bits = 0;
-  return EMB_OK;
+  return launch_prefetch(h);
 }
 
 // B1: wait GRADS, owner merge over sources + apply
@@ -1154,9 +1176,10 @@ emb_status_t backward_impl(emb_ctx *h, const float *d_out, double lr, cudaStream
     g.sink_mode = 0;
     // a step whose input had an error updates nothing (decided on the device: deterministic)
     g.skip_mask = EMB_DEVERR_RANGE | EMB_DEVERR_INVALID | EMB_DEVERR_INTERNAL;
+    if (h->pf.requested) CUDA_TRY(h, cudaEventRecord(h->ev_pre, st));
     LAUNCH(h, KID_GRAD_APPLY, st, launch_grad(g, st));
     h->state = 0;
-    return EMB_OK;
+    return launch_prefetch(h);
   }
   emb_status_t r = backward_phase0(h, bad_dout ? nullptr : d_out, lr, st);
   if (r == EMB_OK) r = backward_phase1(h, lr, st);
@@ -1695,6 +1718,20 @@ emb_status_t emb_profile_read(emb_handle_t h, double *ms, int64_t *launches, int
   if (!h) return EMB_ERR_INVALID;
   CUDA_TRY(h, cudaSetDevice(h->device));
   CUDA_TRY(h, cudaDeviceSynchronize());
+  // diagnostics: EMB_PROFILE_TIMELINE=<path prefix> writes every profiled launch (kernel, start, end in
+  // ms from the first profiled launch) to <prefix>.rank<r>.txt
+  if (const char *tl = getenv("EMB_PROFILE_TIMELINE")) {
+    std::string path = std::string(tl) + ".rank" + std::to_string(h->rank) + ".txt";
+    if (FILE *f = fopen(path.c_str(), "w")) {
+      for (size_t i = 0; i < h->prof_kid.size(); ++i) {
+        float t0 = 0, t1 = 0;
+        cudaEventElapsedTime(&t0, h->prof_ev[0], h->prof_ev[2 * i]);
+        cudaEventElapsedTime(&t1, h->prof_ev[0], h->prof_ev[2 * i + 1]);
+        fprintf(f, "%s %.4f %.4f\n", kKernelNames[h->prof_kid[i]], t0, t1);
+      }
+      fclose(f);
+    }
+  }
   for (size_t i = 0; i < h->prof_kid.size(); ++i) {
     float t = 0;
     CUDA_TRY(h, cudaEventElapsedTime(&t, h->prof_ev[2 * i], h->prof_ev[2 * i + 1]));

@@ -131,15 +131,24 @@ def test_group_prefetch_mismatch_and_state(torch):
             return out
 
         dbs = [_device_batches(bts[s], wl, [0] * W) for s in range(4)]
-        before = snapshot()
-        # prefetch step 0's batches, then look up with rank 1's step-1 batch instead
-        grp.lookup_prefetch([d.ids for d in dbs[0]], [d.offsets for d in dbs[0]], [d.batch for d in dbs[0]],
-                            [d.nnz for d in dbs[0]])
+        pf = lambda d: grp.lookup_prefetch([x.ids for x in d], [x.offsets for x in d],  # noqa: E731
+                                           [x.batch for x in d], [x.nnz for x in d])
+        # a request with no backward before the lookup launched nothing: dropped, the lookup is plain
+        ora = O.OracleEmbedding(cfg1)
+        pf(dbs[1])
         with pytest.raises(EmbError) as ei:
-            grp.lookup_prefetch([d.ids for d in dbs[0]], [d.offsets for d in dbs[0]], [d.batch for d in dbs[0]],
-                                [d.nnz for d in dbs[0]])
+            pf(dbs[1])
         assert ei.value.status == EMB_ERR_STATE
-        mixed = [dbs[0][0], dbs[1][1]]
+        _step(grp, dbs[0], wl.lr, torch)
+        Yo = ora.lookup([(b.ids, b.offsets, b.batch) for b in bts[0]])
+        for r in range(W):
+            assert C.close(dbs[0][r].out.cpu().numpy(), Yo[r]), f"step 0 rank {r}: Y mismatch"
+        # prefetch step 1, launched by step 0's backward; then rank 1 looks up other inputs
+        pf(dbs[1])
+        grp.backward_update([d.dy for d in dbs[0]], wl.lr)
+        torch.cuda.synchronize()
+        before = snapshot()
+        mixed = [dbs[1][0], dbs[2][1]]
         with pytest.raises(EmbError) as ei:
             _step(grp, mixed, wl.lr, torch)
         assert ei.value.status == EMB_ERR_INVALID
@@ -154,6 +163,12 @@ def test_group_prefetch_mismatch_and_state(torch):
             grp.layers[r].clear_error()
         # steps 2 (plain) and 3 (prefetched during step 2's backward) match the oracle
         ora = O.OracleEmbedding(cfg1)
+        for r in range(W):  # (resync: the oracle starts from the GPU's state after step 0)
+            mine = np.concatenate([C.owned_touched(cfg1, cfgW, bts[s], r)[0] for s in (2, 3)])
+            mine = np.unique(mine)
+            if mine.size:
+                t_of = np.searchsorted(cfg1.base, mine, side="right") - 1
+                ora.load_rows(mine, *C.read_owned(grp.layers[r], cfg1, mine, t_of, wl.dim))
         for s in (2, 3):
             _step(grp, dbs[s], wl.lr, torch)
             Yo = ora.lookup([(b.ids, b.offsets, b.batch) for b in bts[s]])
