@@ -482,7 +482,20 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
     if (j < ntile) issue(j, j, meta[j], kk[j], rr[j], uu[j], __shfl_sync(0xffffffffu, kk[j + 1], 0));
     cp_async_commit();
   }
-  uint32_t k2 = kk[NS], r2 = rr[NS], u2 = uu[NS], k3 = kk[NS + 1], p3 = pp[NS + 1];
+  // metadata slots by tile parity (NS even, tb a multiple of NS: the slot of tiles ti + NS and
+  // ti + NS + 2 is s & 1, that of ti + NS + 1 the other one -- compile-time indices). A rotation
+  // k2 = k3, k3 = k4 after the loads instead compiled to register moves that waited on the loads just
+  // issued: 24% of k_grad's stall samples sat on two such moves (profiles/r02_ncu_w1_c2.txt).
+  static_assert(NS % 2 == 0, "metadata slots assume an even stage count");
+  uint32_t KS[2], PS[2], RS[2], US[2];
+  KS[0] = kk[NS];
+  RS[0] = rr[NS];
+  US[0] = uu[NS];
+  PS[0] = 0;
+  KS[1] = kk[NS + 1];
+  PS[1] = pp[NS + 1];
+  RS[1] = 0;
+  US[1] = 0;
 
   DAcc<CPL> acc;
 #pragma unroll
@@ -600,18 +613,13 @@ __global__ void __launch_bounds__(256, MINB) k_grad(const __grid_constant__ Grad
         open = false;
       }
       __syncwarp();  // every lane is done reading the stage before it is refilled
-      if (ti + NS < ntile) issue(ti + NS, s, m, k2, r2, u2, __shfl_sync(0xffffffffu, k3, 0));
+      const int c = s & 1, o = c ^ 1;  // (s is the unrolled stage index: compile-time after unrolling)
+      if (ti + NS < ntile) issue(ti + NS, s, m, KS[c], RS[c], US[c], __shfl_sync(0xffffffffu, KS[o], 0));
       cp_async_commit();  // (possibly empty) group keeps the wait_group accounting uniform
       // advance the metadata pipeline: rows of tile ti+NS+1, keys of tile ti+NS+2
-      const uint32_t r3 = load_row(k3, p3);
-      const uint32_t u3 = load_uo(ti + NS + 1);
-      uint32_t k4, p4;
-      load_kp(ti + NS + 2, k4, p4);
-      k2 = k3;
-      r2 = r3;
-      u2 = u3;
-      k3 = k4;
-      p3 = p4;
+      RS[o] = load_row(KS[o], PS[o]);
+      US[o] = load_uo(ti + NS + 1);
+      load_kp(ti + NS + 2, KS[c], PS[c]);
     }
   }
   cp_async_wait<0>();
