@@ -71,17 +71,38 @@ __device__ __forceinline__ void group_bounds(const SegSortArgs &a, int g, int64_
 // the sorted key range of one CTA: items in sorted order are keys[pa[i]] (table-local ids; `rows` =
 // invalid) with occurrence glo + ia[pa[i]], at sorted positions pos0 + i, i < n
 struct SortedRange {
+  bool redo = false;  // SMEM pass only: the range exceeds the shared-memory buffers (run the global one)
   uint32_t n = 0;
   int64_t pos0 = 0, glo = 0;
   const uint32_t *keys = nullptr, *pa = nullptr, *ia = nullptr;
   uint32_t base = 0, rows = 0;
 };
 
+// SMEM: the range's buffers are in shared memory (n <= SEG_CHUNK_CAP, else it returns redo), so every
+// access compiles to LDS / STS; a runtime choice between shared and global buffers made them all
+// generic LD / ST. !SMEM: global scratch (oversized ranges, rare).
+// the body's static shared memory, one copy for both instantiations
+struct SortShared {
+  uint32_t cnt[SS_WARPS][256];
+  uint32_t part[SS_THREADS / 32];
+  uint32_t wbelow[SS_WARPS], wmine[SS_WARPS];
+  uint32_t kmin, kmax;  // key span of the range (the radix passes sort key - min)
+};
+__device__ __forceinline__ SortShared &sort_shared() {
+  __shared__ SortShared ss;
+  return ss;
+}
+
+template <bool SMEM>
 __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, int work) {
   extern __shared__ __align__(16) uint32_t sm[];
-  __shared__ uint32_t cnt[SS_WARPS][256];
-  __shared__ uint32_t part[SS_THREADS / 32];
-  __shared__ uint32_t wbelow[SS_WARPS], wmine[SS_WARPS];
+  SortShared &ss = sort_shared();
+  auto &cnt = ss.cnt;
+  auto &part = ss.part;
+  auto &wbelow = ss.wbelow;
+  auto &wmine = ss.wmine;
+  uint32_t &s_kmin = ss.kmin;
+  uint32_t &s_kmax = ss.kmax;
   SortedRange out;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int K = a.K;
@@ -130,8 +151,33 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
   const bool staged = ng <= (uint32_t)SEG_CAP;
   uint32_t *gk = sm + 4 * SEG_CHUNK_CAP;  // [SEG_CAP] after the range buffers
   if (staged) {
-#pragma unroll 4
-    for (uint32_t i = tid; i < ng; i += SS_THREADS) gk[i] = local_of(a.ids[glo + i]);
+    // 16-byte loads (two ids each), all of a thread's loads in flight before the first store: 8-byte
+    // loads four deep made this staging ~12% of the kernel's stall samples (profiles/r02_ncu_sort_*.txt).
+    // Clamped (unpredicated) loads, as in k_pool.
+    const int64_t *src = a.ids + glo;
+    const uint32_t h = min((uint32_t)(((uintptr_t)src >> 3) & 1u), ng);  // a leading id to reach 16-B alignment
+    const uint32_t npair = (ng - h) / 2;
+    if (tid == 0) {
+      if (h) gk[0] = local_of(src[0]);
+      if ((ng - h) & 1u) gk[ng - 1] = local_of(src[ng - 1]);
+    }
+    if (npair > 0) {
+      const longlong2 *src2 = reinterpret_cast<const longlong2 *>(src + h);
+      constexpr int U = 16;
+      for (uint32_t p0 = tid; p0 < npair; p0 += SS_THREADS * U) {
+        longlong2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldg(src2 + min(p0 + (uint32_t)u * SS_THREADS, npair - 1u));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t p = p0 + (uint32_t)u * SS_THREADS;
+          if (p < npair) {
+            gk[h + 2 * p] = local_of(v[u].x);
+            gk[h + 2 * p + 1] = local_of(v[u].y);
+          }
+        }
+      }
+    }
     __syncthreads();
   }
   auto key_at = [&](uint32_t i) -> uint32_t { return staged ? gk[i] : local_of(a.ids[glo + i]); };
@@ -152,7 +198,6 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
     mine += __popc(__ballot_sync(0xffffffffu, bb == (uint32_t)bkt));
   }
   if (bkt == 0 && __any_sync(0xffffffffu, badid) && lane == 0) atomicOr(a.err, EMB_DEVERR_RANGE);  // (R4)
-  __shared__ uint32_t s_kmin, s_kmax;  // key span of this range (the radix passes sort key - min)
   if (lane == 0) {
     wbelow[w] = below;
     wmine[w] = mine;
@@ -170,7 +215,11 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
   }
   if (n == 0) return out;
   uint32_t *keys, *ia, *ib;
-  if (n <= SEG_CHUNK_CAP) {
+  if (SMEM) {
+    if (n > SEG_CHUNK_CAP) {
+      out.redo = true;
+      return out;
+    }
     keys = sm;
     ia = sm + n;
     ib = sm + 2 * n;
@@ -219,7 +268,7 @@ __device__ __forceinline__ SortedRange segsort_range_body(const SegSortArgs &a, 
   const int npass = (int)((min(bits, bits_span(s_kmax - kmin)) + 7) / 8);
   // sort item ordinals 0..n-1 (ping-pong pa/pb); keys[] and ia[] stay in place
   uint32_t *pa = ib;
-  uint32_t *pb = (n <= SEG_CHUNK_CAP) ? sm + 3 * n : a.run_k + glo + out_lo;
+  uint32_t *pb = SMEM ? sm + 3 * n : a.run_k + glo + out_lo;
   for (int pass = 0; pass < npass; ++pass) {
     const int shift = 8 * pass;
     for (int d = lane; d < 256; d += 32) cnt[w][d] = 0;
@@ -448,12 +497,23 @@ __global__ void __launch_bounds__(SS_THREADS) k_segsort_range(const __grid_const
     __syncthreads();
     work = (int)s_work;
   }
-  const SortedRange r = segsort_range_body(a, work);  // (block-uniform)
-  if (a.route) {
+  const SortedRange r = segsort_range_body<true>(a, work);  // (block-uniform)
+  if (!r.redo) {
+    if (a.route) {
+      __syncthreads();
+      segsort_route(a, r, work);
+    } else {
+      segsort_write(a, r);
+    }
+  } else {  // (validation and staging repeat: idempotent)
     __syncthreads();
-    segsort_route(a, r, work);
-  } else {
-    segsort_write(a, r);
+    const SortedRange rg = segsort_range_body<false>(a, work);
+    if (a.route) {
+      __syncthreads();
+      segsort_route(a, rg, work);
+    } else {
+      segsort_write(a, rg);
+    }
   }
   if (a.fin) {
     __syncthreads();
