@@ -336,11 +336,15 @@ def run_workload(wl, args, n, rank, local_rank, nccl_id, barrier, e2e_steps, pro
                        device=local_rank)
     stream = torch.cuda.current_stream()
     # emb_lookup_prefetch: the next step's first phase (W = 1: the dedup sort; W > 1: sort + route)
-    # enqueued before this step's backward, so it overlaps the gradient passes (a training loop knows
-    # its next batch). Default on; EMB_BENCH_PREFETCH=0 turns it off. Within each loop the first step
-    # runs its own first phase and the last prefetches nothing, so every step's work is inside the
-    # loop that times it.
-    use_prefetch = os.environ.get("EMB_BENCH_PREFETCH", "1") == "1"
+    # declared before this step's backward, which launches it right after its gradient kernel, so it
+    # overlaps the gradient passes (a training loop knows its next batch). Default: on, except at
+    # N = 2, where the sort's SM time costs the two short gradient passes more than it hides (C3:
+    # 281.7 us/step without, 289.8 with; W = 4: 372.3 without, 361.2 with; C2: 137.0 without, 124-125
+    # with -- profiles/r02_bench_*prefetch*). EMB_BENCH_PREFETCH=0/1 overrides. Within each loop the
+    # first step runs its own first phase and the last prefetches nothing, so every step's work is
+    # inside the loop that times it.
+    pf_env = os.environ.get("EMB_BENCH_PREFETCH")
+    use_prefetch = (pf_env == "1") if pf_env is not None else n != 2
 
     def step(i, last=False):
         db = dev_batches[i % nstage]
