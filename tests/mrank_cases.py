@@ -38,6 +38,9 @@ def case_workload(case, world):
     if case == "hot":  # hot ids (C5 structure, bag 8), mean pooling, SGD
         wl = synthgen.WORKLOADS["C5"].with_(bag_len=8, pool="mean", opt="sgd")
         return wl, 256, 3
+    if case == "skew":  # a 5-row table: one sort range of > 8,192 ids (shared-memory cap) -> global-scratch path
+        wl = synthgen.WORKLOADS["C3"].with_(rows=(5, 60_000), slot_table=(0, 1), dim=16)
+        return wl, 10_000, 2
     if case == "c5":  # C5 exactly (bag 64, 90% of ids in the per-table top 1000), reduced batch
         wl = synthgen.WORKLOADS["C5"]
         return wl, 256, 2

@@ -92,7 +92,8 @@ def _run_group(torch, case, world, shard="cyclic", devices=None, prefetch=False)
     ("c5", 2, "cyclic"), ("c3full", 2, "cyclic"), ("c3full", 4, "cyclic"),
     # W = 8 (BJ:9-11's GPU count) and 16 (EMB_MAX_WORLD) emulated on one GPU: 3- and 4-pass merge
     # trees, 8- / 16-way regions and flags
-    ("c3", 8, "cyclic"), ("hot", 8, "block"), ("gen", 8, "cyclic"), ("c3rw", 8, "cyclic"), ("c3", 16, "cyclic")])
+    ("c3", 8, "cyclic"), ("hot", 8, "block"), ("gen", 8, "cyclic"), ("c3rw", 8, "cyclic"), ("c3", 16, "cyclic"),
+    ("skew", 2, "cyclic")])
 def test_group_row_sharded_parity(torch, case, world, shard):
     _run_group(torch, case, world, shard)
 
