@@ -251,9 +251,9 @@ def test_determinism_bitwise(torch):
 
 @pytest.mark.parametrize("wname", ["C2", "C5"])
 def test_prefetch_matches_plain_bitwise_and_oracle(torch, wname):
-    """emb_lookup_prefetch (the next step's sort enqueued before this step's backward, overlapping it)
-    gives bitwise the same Y and rows as the plain path, and matches the oracle; a prefetch whose
-    inputs differ from the next lookup's is discarded."""
+    """emb_lookup_prefetch (the next step's sort, declared before this step's backward and launched by
+    it, overlapping the gradient pass) gives bitwise the same Y and rows as the plain path, and matches
+    the oracle; a prefetch whose inputs differ from the next lookup's is discarded."""
     from paper_2112_02752_b200.harness import DeviceBatch
     wl = synthgen.WORKLOADS[wname]
     B = 2048 if wname == "C2" else 128
