@@ -216,7 +216,8 @@ class EmbeddingLayer:
                                      _stream(stream, self.device)), "emb_lookup")
 
     def lookup_prefetch(self, ids, offsets, batch: int, nnz: int, stream=None):
-        """Start the dedup sort of the NEXT lookup's inputs so it overlaps this step's backward (W = 1)."""
+        """Declare the NEXT lookup's inputs: the next backward launches their dedup sort (W > 1: sort +
+        route) right after its gradient kernel, overlapping it (include/emb.h emb_lookup_prefetch)."""
         self._check(lib().emb_lookup_prefetch(self.h, _ptr(ids), _ptr(offsets), int(batch), int(nnz),
                                               _stream(stream, self.device)), "emb_lookup_prefetch")
 
