@@ -13,10 +13,10 @@ cur = None
 for l in lines[start + 1:]:
     if l.startswith(".text.") or l.startswith("//---"):
         break
-    m = re.search(r'line (\d+)', l)
-    if "## File" in l and m:
-        if "inlined at" not in l:
-            cur = int(m.group(1))
+    m = re.search(r'## File "([^"]+)", line (\d+)', l)
+    if m:
+        if "inlined at" not in l:  # (file, line): the same line number in different headers must not merge
+            cur = (m.group(1).rsplit("/", 1)[-1], int(m.group(2)))
         continue
     m = re.match(r'\s*/\*([0-9a-f]{4,})\*/', l)
     if m:
@@ -37,7 +37,8 @@ for a, n, s in data:
     agg_i[ln] += n
     agg_s[ln] += s
 ti_, ts_ = sum(agg_i.values()), sum(agg_s.values())
-src = open(sys.argv[4]).read().splitlines() if len(sys.argv) > 4 else None
-for ln in sorted(agg_i, key=lambda k: -agg_i[k])[:30]:
-    txt = src[ln - 1].strip()[:80] if (src and ln) else ""
-    print("L%-5s inst %5.1f%%  stall %5.1f%%  %s" % (ln, 100 * agg_i[ln] / ti_, 100 * agg_s[ln] / ts_, txt))
+src = open(sys.argv[4]).read().splitlines() if len(sys.argv) > 4 else None  # optional: the main source
+for key in sorted(agg_i, key=lambda k: -agg_i[k])[:30]:
+    f, ln = key if key else ("?", 0)
+    txt = src[ln - 1].strip()[:80] if (src and ln and len(sys.argv) > 4 and sys.argv[4].endswith(f)) else ""
+    print("%s:%-5s inst %5.1f%%  stall %5.1f%%  %s" % (f, ln, 100 * agg_i[key] / ti_, 100 * agg_s[key] / ts_, txt))
