@@ -260,7 +260,10 @@ cudaError_t launch_rows_scatter(float *dst, const int64_t *rows, int64_t n, int3
                                 cudaStream_t st);
 
 // per-table stable sort (world == 1 fast path), see segsort.cu
-constexpr int64_t SEG_CAP = 16384;
+// ids of one table group staged in shared memory by every sort CTA of the group (above: read from
+// global memory in both scans). 20,480 covers C1's single group (~18.4K ids: 16,384 left it unstaged,
+// 36 us per sort); 8,192 x 16 B of range buffers + 80 KB + 17 KB static = 225 KB of the 227 KB per CTA
+constexpr int64_t SEG_CAP = 20480;
 constexpr int64_t SEG_BIG = 65536;  // average ids per table group above which the general sort path runs
 struct SegSortArgs {
   const int64_t *ids;       // [nnz] table-local ids in CSR order (validated here: out of range = invalid)
