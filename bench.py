@@ -183,8 +183,12 @@ def oracle_time(wl, budget_s=15.0, max_steps=None, batch=None):
     B = batch or wl.batch
     done, samples, t_tot, nnz = 0, 0, 0.0, 0
     k = 0
+    # a few distinct batches generated up front and cycled (generating one per step cost more wall
+    # time than the oracle step itself at small batches and long --steps)
+    nb = 4 if max_steps is None else max(1, min(4, max_steps))
+    batches = [synthgen.make_batch(wl, rank=0, step=1000 + i, batch=B) for i in range(nb)]
     while t_tot < budget_s and (max_steps is None or done < max_steps):
-        bt = synthgen.make_batch(wl, rank=0, step=1000 + k, batch=B)
+        bt = batches[k % nb]
         t0 = time.perf_counter()
         ora.lookup([(bt.ids, bt.offsets, bt.batch)])
         ora.backward_update([bt.dy], wl.lr)
@@ -240,7 +244,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        per_step = 9e-5 * 26 / wl.num_slots  # ~s per sample of the oracle (dev-host estimate)
+        per_step = 1.3e-4 * 26 / wl.num_slots  # ~s per sample of the oracle (GPU-box host, C2: ~8 k samples/s)
         B = int(max(64, min(wl.batch, 150.0 / max(1, args.steps + args.warmup) / per_step)))
         sps, lps, sample = oracle_time(wl, budget_s=1e9, max_steps=args.steps + args.warmup, batch=B)
         thr, pool = cpu_threads()
